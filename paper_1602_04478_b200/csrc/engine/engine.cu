@@ -1,0 +1,905 @@
+// B200 colour-coding engine (see engine.hpp for the design summary).
+#include "engine.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cub/device/device_scan.cuh>
+#include <map>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../host/errors.hpp"
+#include "sig.cuh"
+
+namespace mb {
+
+// ----------------------------------------------------------------- helpers
+
+#define MB_CUDA(call)                                                                  \
+  do {                                                                                 \
+    cudaError_t _e = (call);                                                           \
+    if (_e != cudaSuccess)                                                             \
+      ::mb::fail(::mb::kCuda, std::string(#call) + ": " + cudaGetErrorString(_e));     \
+  } while (0)
+
+using u64 = unsigned long long;
+
+struct DBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DBuf() = default;
+  explicit DBuf(size_t b) { alloc(b); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr, o.bytes = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    release();
+    p = o.p, bytes = o.bytes;
+    o.p = nullptr, o.bytes = 0;
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void alloc(size_t b) {
+    release();
+    if (b) MB_CUDA(cudaMalloc(&p, b));
+    bytes = b;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+__constant__ SigLut c_lut;
+
+namespace {
+
+uint64_t binom_host(int n, int r) {
+  if (r < 0 || r > n) return 0;
+  uint64_t b = 1;
+  for (int i = 1; i <= r; ++i) b = b * (n - r + i) / i;
+  return b;
+}
+
+// Device-side LUT holder; initialised once per process.
+struct LutHolder {
+  DBuf unrank;
+  bool ready = false;
+  void init() {
+    if (ready) return;
+    std::vector<uint16_t> masks;
+    SigLut L{};
+    for (int t = 0; t <= kMaxColors; ++t) {
+      L.off[t] = static_cast<uint32_t>(masks.size());
+      for (uint32_t m = 0; m < (1u << kMaxColors); ++m)
+        if (__builtin_popcount(m) == t) masks.push_back(static_cast<uint16_t>(m));
+    }
+    L.off[kMaxColors + 1] = static_cast<uint32_t>(masks.size());
+    for (int c = 0; c <= kMaxColors; ++c)
+      for (int i = 0; i <= kMaxColors + 1; ++i) L.binom[c][i] = static_cast<uint32_t>(binom_host(c, i));
+    unrank.alloc(masks.size() * sizeof(uint16_t));
+    MB_CUDA(cudaMemcpy(unrank.p, masks.data(), masks.size() * sizeof(uint16_t),
+                       cudaMemcpyHostToDevice));
+    L.unrank = unrank.as<uint16_t>();
+    MB_CUDA(cudaMemcpyToSymbol(c_lut, &L, sizeof(L)));
+    ready = true;
+  }
+};
+
+LutHolder& lut_holder() {
+  static LutHolder h;
+  return h;
+}
+
+// Checked arithmetic: the reference throws OverflowError (errors.hpp:52); the
+// device raises a flag that the host turns into the same error.
+__device__ __forceinline__ uint64_t mul_ck(uint64_t a, uint64_t b, int* err) {
+  if (__umul64hi(a, b)) atomicOr(err, 1);
+  return a * b;
+}
+
+__device__ __forceinline__ void atomic_add_ck(u64* p, uint64_t v, int* err) {
+  const u64 old = atomicAdd(p, static_cast<u64>(v));
+  if (old + v < old) atomicOr(err, 1);
+}
+
+__device__ __forceinline__ uint64_t add_ck(uint64_t a, uint64_t b, int* err) {
+  const uint64_t r = a + b;
+  if (r < a) atomicOr(err, 1);
+  return r;
+}
+
+// ------------------------------------------------------- graph preprocessing
+
+__global__ void k_slot_rows(uint32_t n, const uint64_t* __restrict__ off, uint32_t* __restrict__ src) {
+  const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= n) return;
+  for (uint64_t e = off[v]; e < off[v + 1]; ++e) src[e] = v;
+}
+
+// rev[e] = slot of (v -> u) for e = (u -> v).
+__global__ void k_reverse_slots(uint64_t m2, const uint64_t* __restrict__ off,
+                                const uint32_t* __restrict__ adj, const uint32_t* __restrict__ src,
+                                uint32_t* __restrict__ rev) {
+  const uint64_t e = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (e >= m2) return;
+  const uint32_t u = src[e], v = adj[e];
+  uint64_t lo = off[v], hi = off[v + 1];
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (adj[mid] < u) lo = mid + 1; else hi = mid;
+  }
+  rev[e] = static_cast<uint32_t>(lo);
+}
+
+__global__ void k_recolor(uint64_t total, const uint8_t* __restrict__ in, uint8_t* __restrict__ out,
+                          int k, int* err) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= total) return;
+  const int c = in[i];
+  if (c < 1 || c > k) atomicOr(err, 2);
+  out[i] = static_cast<uint8_t>(c - 1);
+}
+
+// Degree-ordered orientation: out(x) = neighbours ranked below x, kept in id
+// order, remembered with their CSR slot.
+__global__ void k_out_degree(uint32_t n, const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                             const uint32_t* __restrict__ rank, uint64_t* __restrict__ outdeg) {
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  const uint32_t rx = rank[x];
+  uint64_t c = 0;
+  for (uint64_t e = off[x]; e < off[x + 1]; ++e) c += rank[adj[e]] < rx;
+  outdeg[x] = c;
+}
+
+__global__ void k_out_fill(uint32_t n, const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                           const uint32_t* __restrict__ rank, const uint64_t* __restrict__ out_off,
+                           uint32_t* __restrict__ out_nbr, uint32_t* __restrict__ out_slot) {
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  const uint32_t rx = rank[x];
+  uint64_t w = out_off[x];
+  for (uint64_t e = off[x]; e < off[x + 1]; ++e) {
+    const uint32_t y = adj[e];
+    if (rank[y] < rx) {
+      out_nbr[w] = y;
+      out_slot[w] = static_cast<uint32_t>(e);
+      ++w;
+    }
+  }
+}
+
+// One thread per oriented edge x->y (position j in out(x)): merge out(x) and
+// out(y); every common z closes the triangle x > y > z.  PASS 0 counts, PASS 1
+// writes {x, y, z, slot(x->y), slot(x->z), slot(y->z)}.
+template <int PASS>
+__global__ void k_triangles(uint32_t n, uint64_t nout, const uint64_t* __restrict__ out_off,
+                            const uint32_t* __restrict__ out_nbr, const uint32_t* __restrict__ out_slot,
+                            const uint32_t* __restrict__ out_src, uint64_t* __restrict__ cnt,
+                            const uint64_t* __restrict__ tri_off, uint32_t* __restrict__ tri) {
+  const uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (j >= nout) return;
+  const uint32_t x = out_src[j], y = out_nbr[j];
+  uint64_t a = out_off[x], ae = out_off[x + 1], b = out_off[y], be = out_off[y + 1];
+  uint64_t c = 0, w = PASS ? tri_off[j] : 0;
+  while (a < ae && b < be) {
+    const uint32_t za = out_nbr[a], zb = out_nbr[b];
+    if (za < zb) {
+      ++a;
+    } else if (zb < za) {
+      ++b;
+    } else {
+      if (PASS) {
+        uint32_t* t = tri + 6 * w;
+        t[0] = x, t[1] = y, t[2] = za;
+        t[3] = out_slot[j], t[4] = out_slot[a], t[5] = out_slot[b];
+        ++w;
+      }
+      ++c, ++a, ++b;
+    }
+  }
+  if (!PASS) cnt[j] = c;
+}
+
+// ------------------------------------------------------------- leaf blocks
+
+struct LeafArgs {
+  const uint64_t* off;
+  const uint32_t* adj;
+  const uint32_t* rev;
+  const uint8_t* chi;
+  const uint64_t* ua;  // node child on the boundary a (row = img a), may be null
+  const uint64_t* ub;  // node child on the leaf b (row = img b), may be null
+  const uint64_t* ue;  // edge child (edge table), may be null
+  uint32_t Pa, Pb, Pe, PZ, Pout;
+  int sa, sb, se, sZ;
+  int e_rev;           // edge child stored keyed (b, a): read rev[slot]
+  uint64_t* out;       // unary [n][Pout]
+  int* err;
+  u64* updates;
+};
+
+// Path-table extension along CSR rows (paper §5.2 leaf block: joins of the
+// edge, the leaf's annotation and the boundary's annotation, projected to the
+// boundary).  One GROUP (warp or CTA) per boundary vertex x: the group streams
+// x's neighbour rows (lanes over (neighbour, entry) pairs, so consecutive lanes
+// read consecutive words of a row), folds each into a shared-memory
+// accumulator Z over colour sets, then joins Z with x's own annotation row and
+// writes the output row once.
+template <int GROUP>
+__global__ void __launch_bounds__(GROUP >= 128 ? GROUP : 128)
+leaf_extend_kernel(LeafArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) {
+  extern __shared__ u64 smem[];
+  constexpr int kGroups = (GROUP >= 128 ? GROUP : 128) / GROUP;
+  const int g = threadIdx.x / GROUP, lane = threadIdx.x % GROUP;
+  u64* Z = smem + static_cast<size_t>(g) * (A.PZ + A.Pout);
+  u64* O = Z + A.PZ;
+  const uint32_t gi = blockIdx.x * kGroups + g;
+  const bool active = gi < nv;
+  const uint32_t x = active ? vlist[gi] : 0;
+  uint64_t upd = 0;
+  for (uint32_t i = lane; i < A.PZ + A.Pout; i += GROUP) Z[i] = 0;
+  if (GROUP == 32) __syncwarp(); else __syncthreads();
+  if (active) {
+    const uint32_t cx = A.chi[x], fx = 1u << cx;
+    const uint64_t base = A.off[x], deg = A.off[x + 1] - base;
+    const uint32_t pe = A.ue ? A.Pe : 1u, pb = A.ub ? A.Pb : 1u, per = pe * pb;
+    const uint64_t items = deg * per;
+    for (uint64_t it = lane; it < items; it += GROUP) {
+      const uint64_t j = it / per;
+      const uint32_t r = static_cast<uint32_t>(it - j * per);
+      const uint32_t ie = r / pb, ib = r - ie * pb;
+      const uint64_t slot = base + j;
+      const uint32_t y = __ldg(A.adj + slot);
+      const uint32_t cy = __ldg(A.chi + y), fy = 1u << cy;
+      if (cy == cx) continue;
+      uint32_t M = fx | fy;
+      uint64_t val = 1;
+      if (A.ue) {
+        const uint64_t e = A.e_rev ? __ldg(A.rev + slot) : slot;
+        const uint64_t v = __ldg(A.ue + e * A.Pe + ie);
+        if (!v) continue;
+        M = sig_expand(sig_unrank(c_lut, A.se - 2, ie), fx | fy);
+        val = v;
+      }
+      if (A.ub) {
+        const uint64_t v = __ldg(A.ub + static_cast<uint64_t>(y) * A.Pb + ib);
+        if (!v) continue;
+        const uint32_t Mb = sig_expand(sig_unrank(c_lut, A.sb - 1, ib), fy);
+        if ((M & Mb) != fy) continue;
+        M |= Mb;
+        val = mul_ck(val, v, A.err);
+      }
+      atomic_add_ck(&Z[sig_index(c_lut, M, fx)], val, A.err);
+      ++upd;
+    }
+  }
+  if (GROUP == 32) __syncwarp(); else __syncthreads();
+  if (active) {
+    const uint32_t cx = A.chi[x], fx = 1u << cx;
+    if (!A.ua) {
+      for (uint32_t i = lane; i < A.Pout; i += GROUP) A.out[static_cast<uint64_t>(x) * A.Pout + i] = Z[i];
+    } else {
+      const uint64_t items = static_cast<uint64_t>(A.PZ) * A.Pa;
+      for (uint64_t it = lane; it < items; it += GROUP) {
+        const uint32_t iz = static_cast<uint32_t>(it / A.Pa), ia = static_cast<uint32_t>(it - iz * A.Pa);
+        const uint64_t z = Z[iz];
+        if (!z) continue;
+        const uint64_t a = __ldg(A.ua + static_cast<uint64_t>(x) * A.Pa + ia);
+        if (!a) continue;
+        const uint32_t Mz = sig_expand(sig_unrank(c_lut, A.sZ - 1, iz), fx);
+        const uint32_t Ma = sig_expand(sig_unrank(c_lut, A.sa - 1, ia), fx);
+        if ((Mz & Ma) != fx) continue;
+        atomic_add_ck(&O[sig_index(c_lut, Mz | Ma, fx)], mul_ck(z, a, A.err), A.err);
+        ++upd;
+      }
+      if (GROUP == 32) __syncwarp(); else __syncthreads();
+      for (uint32_t i = lane; i < A.Pout; i += GROUP) A.out[static_cast<uint64_t>(x) * A.Pout + i] = O[i];
+    }
+  }
+  if (upd) atomicAdd(A.updates, static_cast<u64>(upd));
+}
+
+// ----------------------------------------------------------- 3-cycle blocks
+
+struct Factor {
+  const uint64_t* tab;
+  uint32_t P;
+  int s;
+  int pos_a, pos_b;  // node factor: pos_b = -1; edge factor keyed (pos_a, pos_b)
+};
+
+struct TriArgs {
+  const uint32_t* tri;  // [ntri][6]
+  uint64_t ntri;
+  const uint32_t* rev;
+  const uint8_t* chi;
+  Factor f[6];
+  int nf;
+  int out_kind;  // 0 scalar, 1 unary, 2 edge
+  int b0, b1;    // boundary positions
+  uint64_t* out;
+  uint32_t Pout;
+  u64* scalar;
+  int* err;
+  u64* updates;
+};
+
+__constant__ uint8_t c_perm[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+
+// All labelled matches of a 3-cycle block whose three images are a
+// degree-ordered triangle x > y > z (paper Eq. 1 with h = the position of x):
+// one thread per (triangle, position assignment).  Node and edge annotations
+// are folded in with the disjoint-union join (S1 n S2 = shared key colours),
+// and the result is accumulated into the block's scalar, unary or edge table.
+__global__ void __launch_bounds__(256) triangle_block_kernel(TriArgs A) {
+  const uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  uint64_t local = 0, upd = 0;
+  if (w < A.ntri * 6) {
+    const uint64_t t = w / 6;
+    const int p = static_cast<int>(w - t * 6);
+    const uint32_t* T = A.tri + 6 * t;
+    const uint32_t vtx[3] = {T[0], T[1], T[2]};
+    const uint32_t col[3] = {A.chi[vtx[0]], A.chi[vtx[1]], A.chi[vtx[2]]};
+    if (col[0] != col[1] && col[0] != col[2] && col[1] != col[2]) {
+      int sv[3];  // triangle vertex (0..2) at each cycle position
+      for (int q = 0; q < 3; ++q) sv[q] = c_perm[p][q];
+      auto slot = [&](int a, int b) -> uint64_t {  // a, b triangle vertex indices
+        if (a == 0 && b == 1) return T[3];
+        if (a == 1 && b == 0) return __ldg(A.rev + T[3]);
+        if (a == 0 && b == 2) return T[4];
+        if (a == 2 && b == 0) return __ldg(A.rev + T[4]);
+        if (a == 1 && b == 2) return T[5];
+        return __ldg(A.rev + T[5]);
+      };
+      const uint64_t* row[6];
+      uint32_t fixed[6];
+      bool dead = false;
+      for (int i = 0; i < A.nf; ++i) {
+        const Factor& F = A.f[i];
+        if (F.pos_b < 0) {
+          const int a = sv[F.pos_a];
+          row[i] = F.tab + static_cast<uint64_t>(vtx[a]) * F.P;
+          fixed[i] = 1u << col[a];
+        } else {
+          const int a = sv[F.pos_a], b = sv[F.pos_b];
+          row[i] = F.tab + slot(a, b) * F.P;
+          fixed[i] = (1u << col[a]) | (1u << col[b]);
+        }
+      }
+      // Depth-first over the factors' colour sets with pruning.
+      uint32_t idx[6], mstk[7];
+      uint64_t vstk[7];
+      mstk[0] = (1u << col[0]) | (1u << col[1]) | (1u << col[2]);
+      vstk[0] = 1;
+      int d = 0;
+      if (A.nf > 0) idx[0] = 0;
+      while (!dead) {
+        if (d == A.nf) {
+          const uint32_t M = mstk[d];
+          const uint64_t V = vstk[d];
+          ++upd;
+          if (A.out_kind == 0) {
+            local = add_ck(local, V, A.err);
+          } else if (A.out_kind == 1) {
+            const int a = sv[A.b0];
+            atomic_add_ck(reinterpret_cast<u64*>(A.out) + static_cast<uint64_t>(vtx[a]) * A.Pout +
+                              sig_index(c_lut, M, 1u << col[a]),
+                          V, A.err);
+          } else {
+            const int a = sv[A.b0], b = sv[A.b1];
+            atomic_add_ck(reinterpret_cast<u64*>(A.out) + slot(a, b) * A.Pout +
+                              sig_index(c_lut, M, (1u << col[a]) | (1u << col[b])),
+                          V, A.err);
+          }
+          if (d == 0) break;
+          --d;
+          ++idx[d];
+          continue;
+        }
+        const Factor& F = A.f[d];
+        if (idx[d] >= F.P) {
+          if (d == 0) break;
+          --d;
+          ++idx[d];
+          continue;
+        }
+        const uint64_t v = __ldg(row[d] + idx[d]);
+        if (v) {
+          const int f = mb_popc(fixed[d]);
+          const uint32_t Mf = sig_expand(sig_unrank(c_lut, F.s - f, idx[d]), fixed[d]);
+          if ((Mf & mstk[d]) == fixed[d]) {
+            mstk[d + 1] = mstk[d] | Mf;
+            vstk[d + 1] = mul_ck(vstk[d], v, A.err);
+            ++d;
+            if (d < A.nf) idx[d] = 0;
+            continue;
+          }
+        }
+        ++idx[d];
+      }
+    }
+  }
+  if (A.out_kind == 0) {
+    // warp reduce with overflow detection, one atomic per warp
+    for (int o = 16; o > 0; o >>= 1) {
+      const uint64_t other = __shfl_down_sync(0xffffffffu, local, o);
+      local = add_ck(local, other, A.err);
+    }
+    if ((threadIdx.x & 31) == 0 && local) atomic_add_ck(A.scalar, local, A.err);
+  }
+  for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(0xffffffffu, upd, o);
+  if ((threadIdx.x & 31) == 0 && upd) atomicAdd(A.updates, static_cast<u64>(upd));
+}
+
+// Total of a table (singleton-root plans, reference engine.cpp:398).
+__global__ void k_table_total(const uint64_t* __restrict__ t, uint64_t count, u64* out, int* err) {
+  uint64_t local = 0;
+  for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
+    local = add_ck(local, t[i], err);
+  for (int o = 16; o > 0; o >>= 1) local = add_ck(local, __shfl_down_sync(0xffffffffu, local, o), err);
+  if ((threadIdx.x & 31) == 0 && local) atomic_add_ck(out, local, err);
+}
+
+unsigned grid_for(uint64_t work, unsigned block) {
+  const uint64_t g = (work + block - 1) / block;
+  return static_cast<unsigned>(std::max<uint64_t>(1, g));
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- the engine
+
+enum class TKind { None, Scalar, Vertex, Edge };
+
+struct DevTable {
+  TKind kind = TKind::None;
+  int s = 0;
+  uint32_t P = 0;
+  uint64_t rows = 0;
+  DBuf buf;
+  uint64_t* data() const { return buf.as<uint64_t>(); }
+};
+
+struct StepPlan {
+  int block = -1;
+  BlockKind kind = BlockKind::Cycle;
+  int L = 0;
+  std::vector<int> node_tab, edge_tab;
+  std::vector<char> edge_fwd;
+  std::vector<int> bpos;
+  int s_out = 0;
+};
+
+struct GpuEngine::Impl {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint32_t n = 0;
+  uint64_t m2 = 0;
+  DBuf off, adj, rank, src, rev, vlight, vheavy;
+  uint32_t nlight = 0, nheavy = 0;
+  // derived: degree-ordered triangle list
+  bool tri_ready = false;
+  uint64_t ntri = 0;
+  DBuf tri;
+  // plan
+  bool plan_bound = false;
+  int k = 0;
+  Plan plan;
+  std::vector<StepPlan> steps;
+  std::vector<DevTable> tables;
+  bool needs_triangles = false;
+  // per-count scratch
+  DBuf chi, chi_in, flags;  // flags: [0] err (int), [1..] scalar (u64), updates (u64)
+  DBuf scratch;
+  // stats / timing
+  EngineStats st;
+  bool timing = false;
+  std::map<std::string, KernelTiming> timings;
+  uint64_t launch_count = 0;
+  std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  std::vector<cudaEvent_t> event_pool;
+
+  cudaEvent_t get_event() {
+    if (!event_pool.empty()) {
+      cudaEvent_t e = event_pool.back();
+      event_pool.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    MB_CUDA(cudaEventCreate(&e));
+    return e;
+  }
+
+  template <class F>
+  void launch(const char* name, F&& f) {
+    cudaEvent_t a = nullptr, b = nullptr;
+    if (timing) {
+      a = get_event();
+      b = get_event();
+      MB_CUDA(cudaEventRecord(a, stream));
+    }
+    f();
+    MB_CUDA(cudaGetLastError());
+    ++launch_count;
+    if (timing) {
+      MB_CUDA(cudaEventRecord(b, stream));
+      pending.push_back({name, {a, b}});
+    }
+  }
+
+  void collect_timings() {
+    for (auto& p : pending) {
+      float ms = 0;
+      MB_CUDA(cudaEventElapsedTime(&ms, p.second.first, p.second.second));
+      auto& t = timings[p.first];
+      t.name = p.first;
+      t.ms += ms;
+      t.launches++;
+      event_pool.push_back(p.second.first);
+      event_pool.push_back(p.second.second);
+    }
+    pending.clear();
+  }
+
+  void upload(const CsrGraph& g) {
+    lut_holder().init();
+    n = g.n;
+    m2 = 2 * g.m;
+    if (m2 >= 0xFFFFFFFFULL) fail(kSpec, "graph exceeds 2^32 half-edges (32-bit CSR slots)");
+    off.alloc((n + 1) * sizeof(uint64_t));
+    adj.alloc(std::max<uint64_t>(m2, 1) * sizeof(uint32_t));
+    MB_CUDA(cudaMemcpyAsync(off.p, g.offsets.data(), (n + 1) * sizeof(uint64_t), cudaMemcpyHostToDevice, stream));
+    if (m2) MB_CUDA(cudaMemcpyAsync(adj.p, g.adj.data(), m2 * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
+    const auto rk = degree_rank(g);
+    rank.alloc(std::max<uint32_t>(n, 1) * sizeof(uint32_t));
+    if (n) MB_CUDA(cudaMemcpyAsync(rank.p, rk.data(), n * sizeof(uint32_t), cudaMemcpyHostToDevice, stream));
+    src.alloc(std::max<uint64_t>(m2, 1) * sizeof(uint32_t));
+    rev.alloc(std::max<uint64_t>(m2, 1) * sizeof(uint32_t));
+    if (n) launch("slot_rows", [&] { k_slot_rows<<<grid_for(n, 256), 256, 0, stream>>>(n, off.as<uint64_t>(), src.as<uint32_t>()); });
+    if (m2)
+      launch("reverse_slots", [&] {
+        k_reverse_slots<<<grid_for(m2, 256), 256, 0, stream>>>(m2, off.as<uint64_t>(), adj.as<uint32_t>(),
+                                                              src.as<uint32_t>(), rev.as<uint32_t>());
+      });
+    // degree bins for the vertex-centric kernels: warp per light vertex,
+    // CTA per heavy vertex (threshold = 8 warp-iterations of a unit row).
+    std::vector<uint32_t> light, heavy;
+    for (uint32_t v = 0; v < n; ++v) (g.degree(v) > 256 ? heavy : light).push_back(v);
+    nlight = static_cast<uint32_t>(light.size());
+    nheavy = static_cast<uint32_t>(heavy.size());
+    vlight.alloc(std::max<size_t>(light.size(), 1) * 4);
+    vheavy.alloc(std::max<size_t>(heavy.size(), 1) * 4);
+    if (nlight) MB_CUDA(cudaMemcpyAsync(vlight.p, light.data(), light.size() * 4, cudaMemcpyHostToDevice, stream));
+    if (nheavy) MB_CUDA(cudaMemcpyAsync(vheavy.p, heavy.data(), heavy.size() * 4, cudaMemcpyHostToDevice, stream));
+    flags.alloc(64);
+    MB_CUDA(cudaStreamSynchronize(stream));
+  }
+
+  void build_triangles() {
+    if (tri_ready) return;
+    DBuf outdeg((n + 1) * sizeof(uint64_t)), out_off((n + 1) * sizeof(uint64_t));
+    MB_CUDA(cudaMemsetAsync(outdeg.p, 0, (n + 1) * sizeof(uint64_t), stream));
+    launch("tri_outdeg", [&] {
+      k_out_degree<<<grid_for(n, 256), 256, 0, stream>>>(n, off.as<uint64_t>(), adj.as<uint32_t>(),
+                                                         rank.as<uint32_t>(), outdeg.as<uint64_t>());
+    });
+    exclusive_scan(outdeg.as<uint64_t>(), out_off.as<uint64_t>(), n + 1);
+    uint64_t nout = 0;
+    MB_CUDA(cudaMemcpyAsync(&nout, out_off.as<uint64_t>() + n, 8, cudaMemcpyDeviceToHost, stream));
+    MB_CUDA(cudaStreamSynchronize(stream));
+    DBuf out_nbr(std::max<uint64_t>(nout, 1) * 4), out_slot(std::max<uint64_t>(nout, 1) * 4),
+        out_src(std::max<uint64_t>(nout, 1) * 4);
+    launch("tri_outfill", [&] {
+      k_out_fill<<<grid_for(n, 256), 256, 0, stream>>>(n, off.as<uint64_t>(), adj.as<uint32_t>(), rank.as<uint32_t>(),
+                                                       out_off.as<uint64_t>(), out_nbr.as<uint32_t>(),
+                                                       out_slot.as<uint32_t>());
+    });
+    // out_src[j] = src[out_slot[j]]
+    gather_src(out_slot.as<uint32_t>(), out_src.as<uint32_t>(), nout);
+    DBuf cnt((nout + 1) * 8), toff((nout + 1) * 8);
+    MB_CUDA(cudaMemsetAsync(cnt.p, 0, (nout + 1) * 8, stream));
+    if (nout)
+      launch("tri_count", [&] {
+        k_triangles<0><<<grid_for(nout, 128), 128, 0, stream>>>(n, nout, out_off.as<uint64_t>(), out_nbr.as<uint32_t>(),
+                                                                out_slot.as<uint32_t>(), out_src.as<uint32_t>(),
+                                                                cnt.as<uint64_t>(), nullptr, nullptr);
+      });
+    exclusive_scan(cnt.as<uint64_t>(), toff.as<uint64_t>(), nout + 1);
+    MB_CUDA(cudaMemcpyAsync(&ntri, toff.as<uint64_t>() + nout, 8, cudaMemcpyDeviceToHost, stream));
+    MB_CUDA(cudaStreamSynchronize(stream));
+    tri.alloc(std::max<uint64_t>(ntri, 1) * 6 * sizeof(uint32_t));
+    if (nout && ntri)
+      launch("tri_fill", [&] {
+        k_triangles<1><<<grid_for(nout, 128), 128, 0, stream>>>(n, nout, out_off.as<uint64_t>(), out_nbr.as<uint32_t>(),
+                                                                out_slot.as<uint32_t>(), out_src.as<uint32_t>(),
+                                                                nullptr, toff.as<uint64_t>(), tri.as<uint32_t>());
+      });
+    MB_CUDA(cudaStreamSynchronize(stream));
+    st.triangles = ntri;
+    tri_ready = true;
+  }
+
+  void exclusive_scan(const uint64_t* in, uint64_t* out, uint64_t count) {
+    size_t tmp = 0;
+    MB_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, in, out, static_cast<int64_t>(count), stream));
+    if (scratch.bytes < tmp) scratch.alloc(tmp);
+    MB_CUDA(cub::DeviceScan::ExclusiveSum(scratch.p, tmp, in, out, static_cast<int64_t>(count), stream));
+  }
+
+  void gather_src(const uint32_t* slots, uint32_t* outp, uint64_t count);
+
+  // ------------------------------------------------------------ plan binding
+
+  static uint64_t binom(int a, int b) { return binom_host(a, b); }
+
+  void bind(const Plan& p, int kk) {
+    if (kk > kMaxColors) fail(kSpec, "GPU engine supports k <= 16 colours");
+    k = kk;
+    plan = p;
+    steps.clear();
+    tables.clear();
+    tables.resize(p.blocks.size());
+    needs_triangles = false;
+    for (int id : p.bottom_up()) {
+      const Block& b = p.blocks[id];
+      StepPlan sp;
+      sp.block = id;
+      sp.kind = b.kind;
+      sp.L = b.size();
+      sp.s_out = __builtin_popcount(p.subquery_nodes(id));
+      for (int c : b.node_child) sp.node_tab.push_back(c);
+      for (int c : b.edge_child) sp.edge_tab.push_back(c);
+      sp.edge_fwd = b.edge_fwd;
+      for (int x : b.boundary) sp.bpos.push_back(b.pos(x));
+      DevTable& out = tables[id];
+      out.s = sp.s_out;
+      const bool is_root = id == p.root;
+      if (b.kind == BlockKind::Leaf || b.boundary.size() == 1) {
+        out.kind = TKind::Vertex;
+        out.P = static_cast<uint32_t>(binom(k - 1, sp.s_out - 1));
+        out.rows = n;
+      } else if (b.boundary.empty()) {
+        out.kind = TKind::Scalar;
+      } else {
+        // two boundary nodes: stored per CSR slot when the pair is always a
+        // graph edge (cycle-adjacent through an original or edge-keyed edge)
+        const int d = (sp.bpos[1] - sp.bpos[0] + sp.L) % sp.L;
+        int e = -1;
+        if (d == 1) e = sp.bpos[0];
+        if (d == sp.L - 1) e = sp.bpos[1];
+        const bool supported = e >= 0 && (sp.edge_tab[e] < 0 || tables[sp.edge_tab[e]].kind == TKind::Edge);
+        if (!supported)
+          fail(kSpec, "plan needs a projection table over non-adjacent vertex pairs (block " + b.canonical() +
+                          "); not yet supported by the GPU engine");
+        out.kind = TKind::Edge;
+        out.P = static_cast<uint32_t>(binom(k - 2, sp.s_out - 2));
+        out.rows = m2;
+      }
+      (void)is_root;
+      if (b.kind == BlockKind::Cycle) {
+        for (int e = 0; e < sp.L; ++e)
+          if (sp.edge_tab[e] >= 0 && tables[sp.edge_tab[e]].kind != TKind::Edge)
+            fail(kSpec, "cycle edge annotated with a non-edge table; not yet supported");
+        if (sp.L == 3) needs_triangles = true;
+        else fail(kSpec, "cycle blocks longer than 3 are not yet supported by the GPU engine");
+      } else if (sp.edge_tab[0] >= 0 && tables[sp.edge_tab[0]].kind != TKind::Edge) {
+        fail(kSpec, "leaf edge annotated with a non-edge table; not yet supported");
+      }
+      if (out.kind == TKind::Vertex || out.kind == TKind::Edge) {
+        out.buf.alloc(std::max<uint64_t>(out.rows * out.P, 1) * sizeof(uint64_t));
+        st.table_bytes += out.buf.bytes;
+      }
+      steps.push_back(std::move(sp));
+    }
+    plan_bound = true;
+  }
+
+  // ---------------------------------------------------------------- solving
+
+  void run_leaf(const StepPlan& sp, int* err, u64* upd) {
+    DevTable& out = tables[sp.block];
+    LeafArgs A{};
+    A.off = off.as<uint64_t>();
+    A.adj = adj.as<uint32_t>();
+    A.rev = rev.as<uint32_t>();
+    A.chi = chi.as<uint8_t>();
+    A.err = err;
+    A.updates = upd;
+    int s_right = 2;
+    if (sp.edge_tab[0] >= 0) {
+      const DevTable& t = tables[sp.edge_tab[0]];
+      A.ue = t.data(), A.Pe = t.P, A.se = t.s, A.e_rev = !sp.edge_fwd[0];
+      s_right = t.s;
+    }
+    if (sp.node_tab[1] >= 0) {
+      const DevTable& t = tables[sp.node_tab[1]];
+      A.ub = t.data(), A.Pb = t.P, A.sb = t.s;
+      s_right += t.s - 1;
+    }
+    if (sp.node_tab[0] >= 0) {
+      const DevTable& t = tables[sp.node_tab[0]];
+      A.ua = t.data(), A.Pa = t.P, A.sa = t.s;
+    }
+    A.sZ = s_right;
+    A.PZ = static_cast<uint32_t>(binom(k - 1, s_right - 1));
+    A.Pout = out.P;
+    A.out = out.data();
+    if (!A.ua && A.PZ != A.Pout) fail(kInternal, "leaf popcount mismatch");
+    const size_t per_group = (A.PZ + (A.ua ? A.Pout : 0)) * sizeof(u64);
+    if (!A.ua) A.Pout = out.P;  // O unused
+    const size_t group_bytes = (A.PZ + A.Pout) * sizeof(u64);
+    (void)per_group;
+    if (group_bytes * 4 > 200 * 1024) fail(kSpec, "leaf table row too wide for shared memory (k too large)");
+    if (nlight) {
+      const size_t smem = group_bytes * 4;  // 4 warps per CTA
+      if (smem > 48 * 1024)
+        MB_CUDA(cudaFuncSetAttribute(leaf_extend_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      launch("leaf_extend", [&] {
+        leaf_extend_kernel<32><<<grid_for(nlight, 4), 128, smem, stream>>>(A, vlight.as<uint32_t>(), nlight);
+      });
+    }
+    if (nheavy) {
+      const size_t smem = group_bytes;
+      if (smem > 48 * 1024)
+        MB_CUDA(cudaFuncSetAttribute(leaf_extend_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      launch("leaf_extend_heavy", [&] {
+        leaf_extend_kernel<256><<<nheavy, 256, smem, stream>>>(A, vheavy.as<uint32_t>(), nheavy);
+      });
+    }
+  }
+
+  void run_triangle(const StepPlan& sp, int* err, u64* scalar, u64* upd) {
+    DevTable& out = tables[sp.block];
+    TriArgs A{};
+    A.tri = tri.as<uint32_t>();
+    A.ntri = ntri;
+    A.rev = rev.as<uint32_t>();
+    A.chi = chi.as<uint8_t>();
+    A.err = err;
+    A.updates = upd;
+    A.scalar = scalar;
+    int nf = 0;
+    for (int q = 0; q < 3; ++q) {
+      if (sp.node_tab[q] >= 0) {
+        const DevTable& t = tables[sp.node_tab[q]];
+        A.f[nf++] = Factor{t.data(), t.P, t.s, q, -1};
+      }
+    }
+    for (int e = 0; e < 3; ++e) {
+      if (sp.edge_tab[e] >= 0) {
+        const DevTable& t = tables[sp.edge_tab[e]];
+        const int a = e, b = (e + 1) % 3;
+        A.f[nf++] = sp.edge_fwd[e] ? Factor{t.data(), t.P, t.s, a, b} : Factor{t.data(), t.P, t.s, b, a};
+      }
+    }
+    A.nf = nf;
+    if (out.kind == TKind::Scalar) {
+      A.out_kind = 0;
+    } else if (out.kind == TKind::Vertex) {
+      A.out_kind = 1;
+      A.b0 = sp.bpos[0];
+    } else {
+      A.out_kind = 2;
+      A.b0 = sp.bpos[0];
+      A.b1 = sp.bpos[1];
+    }
+    A.out = out.data();
+    A.Pout = out.P;
+    if (ntri)
+      launch("triangle_block", [&] { triangle_block_kernel<<<grid_for(ntri * 6, 256), 256, 0, stream>>>(A); });
+  }
+
+  void count(const uint8_t* chi_src, int nc, bool host, uint64_t* result) {
+    if (!plan_bound) fail(kSpec, "no plan bound");
+    if (k == 1) {
+      for (int c = 0; c < nc; ++c) result[c] = n;
+      return;
+    }
+    if (needs_triangles) build_triangles();
+    if (chi.bytes < std::max<uint64_t>(n, 1)) chi.alloc(std::max<uint64_t>(n, 1));
+    int* err = flags.as<int>();
+    u64* scalar = reinterpret_cast<u64*>(flags.as<char>() + 8);
+    u64* upd = reinterpret_cast<u64*>(flags.as<char>() + 16);
+    st.dp_updates = 0;
+    if (host && chi_in.bytes < static_cast<uint64_t>(n) * nc) chi_in.alloc(std::max<uint64_t>(static_cast<uint64_t>(n) * nc, 1));
+    if (host && n)
+      MB_CUDA(cudaMemcpyAsync(chi_in.p, chi_src, static_cast<uint64_t>(n) * nc, cudaMemcpyHostToDevice, stream));
+    const uint8_t* dchi = host ? chi_in.as<uint8_t>() : chi_src;
+    std::vector<uint64_t> host_flags(3 * nc);
+    DBuf res(static_cast<size_t>(nc) * 24);
+    for (int c = 0; c < nc; ++c) {
+      MB_CUDA(cudaMemsetAsync(flags.p, 0, 24, stream));
+      if (n)
+        launch("recolor", [&] {
+          k_recolor<<<grid_for(n, 256), 256, 0, stream>>>(n, dchi + static_cast<uint64_t>(c) * n, chi.as<uint8_t>(), k, err);
+        });
+      for (const StepPlan& sp : steps) {
+        DevTable& out = tables[sp.block];
+        if (out.kind == TKind::Edge || (out.kind == TKind::Vertex && sp.kind == BlockKind::Cycle))
+          MB_CUDA(cudaMemsetAsync(out.buf.p, 0, out.buf.bytes, stream));
+        if (sp.kind == BlockKind::Leaf) run_leaf(sp, err, upd);
+        else run_triangle(sp, err, scalar, upd);
+      }
+      if (plan.singleton_root) {
+        const DevTable& t = tables[plan.root];
+        launch("table_total", [&] {
+          k_table_total<<<296, 256, 0, stream>>>(t.data(), t.rows * t.P, scalar, err);
+        });
+      }
+      MB_CUDA(cudaMemcpyAsync(res.as<char>() + 24 * c, flags.p, 24, cudaMemcpyDeviceToDevice, stream));
+    }
+    MB_CUDA(cudaMemcpyAsync(host_flags.data(), res.p, 24 * static_cast<size_t>(nc), cudaMemcpyDeviceToHost, stream));
+    MB_CUDA(cudaStreamSynchronize(stream));
+    if (timing) collect_timings();
+    for (int c = 0; c < nc; ++c) {
+      const int e = static_cast<int>(host_flags[3 * c] & 0xffffffffu);
+      if (e & 2) fail(kSpec, "colouring has a colour outside 1..k");
+      if (e & 1) fail(kOverflow, "count overflow (64-bit)");
+      result[c] = host_flags[3 * c + 1];
+      st.dp_updates += host_flags[3 * c + 2];
+    }
+  }
+};
+
+namespace {
+__global__ void k_gather_u32(const uint32_t* __restrict__ idx, const uint32_t* __restrict__ src,
+                             uint32_t* __restrict__ out, uint64_t count) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i < count) out[i] = src[idx[i]];
+}
+}  // namespace
+
+void GpuEngine::Impl::gather_src(const uint32_t* slots, uint32_t* outp, uint64_t count) {
+  if (!count) return;
+  launch("gather", [&] { k_gather_u32<<<grid_for(count, 256), 256, 0, stream>>>(slots, src.as<uint32_t>(), outp, count); });
+}
+
+GpuEngine::GpuEngine(const CsrGraph& g, int device) : impl_(new Impl) {
+  impl_->device = device;
+  MB_CUDA(cudaSetDevice(device));
+  MB_CUDA(cudaStreamCreateWithFlags(&impl_->stream, cudaStreamNonBlocking));
+  impl_->upload(g);
+}
+
+GpuEngine::~GpuEngine() {
+  if (!impl_) return;
+  for (auto e : impl_->event_pool) cudaEventDestroy(e);
+  for (auto& p : impl_->pending) {
+    cudaEventDestroy(p.second.first);
+    cudaEventDestroy(p.second.second);
+  }
+  if (impl_->stream) cudaStreamDestroy(impl_->stream);
+}
+
+uint32_t GpuEngine::num_vertices() const { return impl_->n; }
+uint64_t GpuEngine::num_edges() const { return impl_->m2 / 2; }
+void GpuEngine::bind_plan(const Plan& plan, int k) { impl_->bind(plan, k); }
+void GpuEngine::count(const uint8_t* chi, int nc, bool host, uint64_t* out) { impl_->count(chi, nc, host, out); }
+void GpuEngine::reset_derived() {
+  impl_->tri_ready = false;
+  impl_->tri.release();
+}
+void GpuEngine::enable_timing(bool on) {
+  impl_->timing = on;
+  impl_->timings.clear();
+}
+std::vector<GpuEngine::KernelTiming> GpuEngine::kernel_timings() const {
+  std::vector<KernelTiming> v;
+  for (auto& kv : impl_->timings) v.push_back(kv.second);
+  return v;
+}
+uint64_t GpuEngine::launches() const { return impl_->launch_count; }
+const EngineStats& GpuEngine::stats() const { return impl_->st; }
+void* GpuEngine::stream() const { return impl_->stream; }
+
+}  // namespace mb

@@ -1,0 +1,76 @@
+// B200 colour-coding engine: host-side orchestration of the device kernels.
+//
+// Replaces the reference's counting engine (include/motif/engine.hpp:118-123,
+// count_colorful / count_colorful_exec, and the Executor table primitives of
+// engine.hpp:39-65) for every treewidth-2 plan the planner emits.  Projection
+// tables (reference: hash maps, table.hpp:36) live in HBM as dense rows indexed
+// by colour set (sig.cuh):
+//   - unary tables   : one row per vertex           [n][C(k-1, s-1)]
+//   - edge tables    : one row per CSR slot (u->v)  [2m][C(k-2, s-2)]
+//   - scalars        : the root's colourful count
+// Blocks are solved by fused kernels instead of the reference's op-by-op
+// table algebra:
+//   - leaf blocks      -> leaf_extend_kernel   (path-table extension along CSR rows)
+//   - 3-cycle blocks   -> triangle_block_kernel over the degree-ordered triangle list
+//   - longer cycles    -> cycle engine (degree-capped half paths, DB, Eq. 1)
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../host/graph.hpp"
+#include "../host/plan.hpp"
+
+namespace mb {
+
+struct EngineStats {
+  uint64_t triangles = 0;       // degree-ordered triangles listed
+  uint64_t table_bytes = 0;     // bytes of DP tables resident
+  uint64_t dp_updates = 0;      // table-entry updates (nonzero contributions) of the last count
+  double last_ms = 0;
+};
+
+class GpuEngine {
+ public:
+  explicit GpuEngine(const CsrGraph& g, int device = 0);
+  ~GpuEngine();
+  GpuEngine(const GpuEngine&) = delete;
+  GpuEngine& operator=(const GpuEngine&) = delete;
+
+  uint32_t num_vertices() const;
+  uint64_t num_edges() const;
+
+  // Binds a plan (allocates its tables, builds the structures it needs).
+  void bind_plan(const Plan& plan, int k);
+
+  // Colourful count for each colouring.  `chi` holds `count` colourings of n
+  // vertices each, colours 1..k, in host memory (host=true) or device memory.
+  void count(const uint8_t* chi, int count_colorings, bool host, uint64_t* out);
+
+  // Drops plan-derived graph structures (triangle list); the next count
+  // rebuilds them.  Used by the benchmark to keep that work inside a step.
+  void reset_derived();
+
+  // Kernel-level timing hooks for the roofline: average duration (ms) of the
+  // dominant DP kernel over the last count() and its algorithmic bytes.
+  struct KernelTiming {
+    std::string name;
+    double ms = 0;
+    uint64_t bytes = 0;
+    uint64_t launches = 0;
+  };
+  std::vector<KernelTiming> kernel_timings() const;
+  void enable_timing(bool on);
+  uint64_t launches() const;
+  const EngineStats& stats() const;
+  void* stream() const;
+
+  struct Impl;
+
+ private:
+  std::unique_ptr<Impl> impl_;
+};
+
+}  // namespace mb
