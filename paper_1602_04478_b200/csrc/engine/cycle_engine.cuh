@@ -1,0 +1,685 @@
+// General cycle-block solver (any length L >= 3, any node/edge annotations,
+// 0/1/2 boundary nodes).  Included by engine.cu after its helpers.
+//
+// Degree-based (DB) evaluation, reference engine.cpp:337-366 and paper §5.1
+// Eq. 1: every labelled match of the cycle has exactly one position h holding
+// its (degree, id)-highest vertex x.  For each h the cycle is split into two
+// half paths that start at x and meet at a position d; every other image must
+// rank below x (the cap).  The reference splits at d = h + floor(L/2) and
+// records interior boundary images in extra key slots; here d is chosen as a
+// boundary position whenever h is not one (a valid split for Eq. 1 because
+// both halves are rebuilt per h), so at most one boundary image is ever carried
+// as a recorded key.
+//
+// The half-path tables of the reference (keys (x, v[, r]), hash maps) become
+// level-synchronous frontiers on the device: sorted arrays of packed keys
+// (x, v, r) with a dense colour-set row per key.  One hop expands every entry
+// along the CSR row of v (relation = graph edges, optionally weighted by an
+// edge-keyed child table), joins the node annotation of the new position,
+// and aggregates equal keys by a radix sort + segmented add.  The two halves
+// are then merged with the disjoint-union join (S+ n S- = {chi x, chi v}).
+// Anchors are processed in batches so frontier memory stays bounded.
+
+struct TabView {
+  int kind = 0;  // 0 none, 1 scalar, 2 vertex, 3 edge, 4 pair
+  int s = 0;
+  uint32_t P = 0;
+  uint64_t* data = nullptr;
+  // pair tables: CSR by first key (off[n+1], cols) and its transpose
+  const uint64_t* off = nullptr;
+  const uint32_t* cols = nullptr;
+  const uint64_t* off_t = nullptr;
+  const uint32_t* cols_t = nullptr;
+  const uint64_t* data_t = nullptr;
+};
+
+struct GraphView {
+  uint32_t n;
+  uint64_t m2;
+  const uint64_t* off;
+  const uint32_t* adj;
+  const uint32_t* rev;
+  const uint32_t* rank;
+  const uint8_t* chi;
+};
+
+struct HopArgs {
+  GraphView G;
+  // input frontier
+  const uint64_t* key_in;
+  const uint64_t* pay_in;
+  uint64_t n_in;
+  int s_in;
+  uint32_t P_in;
+  int first_hop;  // input keys are (x, x): fixed colours {chi x}
+  int in_has_r;
+  // work decomposition
+  const uint64_t* woff;  // exclusive scan of per-entry degree (n_in + 1)
+  uint64_t W;
+  // hop relation: rows roff/radj (graph CSR or a pair table's CSR)
+  const uint64_t* roff;
+  const uint32_t* radj;
+  const uint64_t* etab;  // relation payload (edge or pair table), may be null
+  uint32_t Pe;
+  int se;
+  int e_rev;
+  const uint64_t* ntab;  // node child at the new position, may be null
+  uint32_t Pn;
+  int sn;
+  int record;            // the new position is the recorded boundary
+  // output contributions
+  int s_out;
+  uint32_t P_out;
+  int out_has_r;
+  int bits;
+  uint64_t* key_out;     // [W]
+  uint64_t* row_out;     // [W][P_out]
+  int* err;
+  u64* updates;
+};
+
+__device__ __forceinline__ uint64_t pack_key(uint64_t x, uint64_t v, uint64_t r, int has_r, int bits) {
+  return has_r ? (((x << bits) | v) << bits) | r : (x << bits) | v;
+}
+
+__device__ __forceinline__ void unpack_key(uint64_t key, int has_r, int bits, uint32_t& x, uint32_t& v,
+                                           uint32_t& r) {
+  const uint64_t mask = (bits >= 64) ? ~0ull : ((1ull << bits) - 1);
+  if (has_r) {
+    r = static_cast<uint32_t>(key & mask);
+    key >>= bits;
+  } else {
+    r = 0xFFFFFFFFu;
+  }
+  v = static_cast<uint32_t>(key & mask);
+  x = static_cast<uint32_t>(key >> bits);
+}
+
+__global__ void k_hop_work(const uint64_t* __restrict__ key_in, uint64_t n_in, int has_r, int bits,
+                           const uint64_t* __restrict__ off, uint64_t* __restrict__ work) {  // off: relation rows
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n_in) return;
+  uint32_t x, v, r;
+  unpack_key(key_in[i], has_r, bits, x, v, r);
+  work[i] = off[v + 1] - off[v];
+}
+
+// One thread per (frontier entry, neighbour) work item; writes the item's key
+// (UINT64_MAX when it contributes nothing) and its dense colour-set row.
+__global__ void __launch_bounds__(256) k_hop_expand(HopArgs A) {
+  const uint64_t item = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (item >= A.W) return;
+  // entry = last i with woff[i] <= item
+  uint64_t lo = 0, hi = A.n_in;
+  while (hi - lo > 1) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (A.woff[mid] <= item) lo = mid; else hi = mid;
+  }
+  const uint64_t i = lo;
+  uint32_t x, v, r;
+  unpack_key(A.key_in[i], A.in_has_r, A.bits, x, v, r);
+  const uint64_t slot = A.roff[v] + (item - A.woff[i]);
+  const uint32_t w = A.radj[slot];
+  uint64_t* row = A.row_out + item * A.P_out;
+  for (uint32_t j = 0; j < A.P_out; ++j) row[j] = 0;
+  uint64_t key = ~0ull;
+  bool any = false;
+  if (A.G.rank[w] < A.G.rank[x]) {
+    const uint32_t cx = A.G.chi[x], cv = A.G.chi[v], cw = A.G.chi[w];
+    const uint32_t fin = A.first_hop ? (1u << cx) : ((1u << cx) | (1u << cv));
+    const uint32_t fout = (1u << cx) | (1u << cw);
+    const uint32_t fw = 1u << cw, fv = 1u << cv;
+    const uint64_t* prow = A.pay_in + i * A.P_in;
+    const int t_in = A.s_in - mb_popc(fin);
+    const uint64_t erow = A.etab ? (A.e_rev ? A.G.rev[slot] : slot) * A.Pe : 0;
+    for (uint32_t ii = 0; ii < A.P_in; ++ii) {
+      const uint64_t pv = prow[ii];
+      if (!pv) continue;
+      const uint32_t Sin = sig_expand(sig_unrank(c_lut, t_in, ii), fin);
+      if (Sin & fw) continue;
+      const uint32_t ne = A.etab ? A.Pe : 1u;
+      for (uint32_t ie = 0; ie < ne; ++ie) {
+        uint32_t S1;
+        uint64_t v1;
+        if (A.etab) {
+          const uint64_t ev = A.etab[erow + ie];
+          if (!ev) continue;
+          const uint32_t E = sig_expand(sig_unrank(c_lut, A.se - 2, ie), fv | fw);
+          if ((E & Sin) != fv) continue;
+          S1 = Sin | E;
+          v1 = mul_ck(pv, ev, A.err);
+        } else {
+          S1 = Sin | fw;
+          v1 = pv;
+        }
+        const uint32_t nn = A.ntab ? A.Pn : 1u;
+        for (uint32_t in = 0; in < nn; ++in) {
+          uint32_t S2;
+          uint64_t v2;
+          if (A.ntab) {
+            const uint64_t nv = A.ntab[static_cast<uint64_t>(w) * A.Pn + in];
+            if (!nv) continue;
+            const uint32_t Nn = sig_expand(sig_unrank(c_lut, A.sn - 1, in), fw);
+            if ((Nn & S1) != fw) continue;
+            S2 = S1 | Nn;
+            v2 = mul_ck(v1, nv, A.err);
+          } else {
+            S2 = S1;
+            v2 = v1;
+          }
+          const uint32_t o = sig_index(c_lut, S2, fout);
+          row[o] = add_ck(row[o], v2, A.err);
+          any = true;
+        }
+      }
+    }
+    if (any) {
+      const uint32_t rr = A.record ? w : r;
+      key = pack_key(x, w, rr, A.out_has_r, A.bits);
+    }
+  }
+  A.key_out[item] = key;
+  if (any) atomicAdd(A.updates, 1ull);
+}
+
+__global__ void k_iota(uint64_t* __restrict__ out, uint64_t W) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i < W) out[i] = i;
+}
+
+__global__ void k_seg_heads(const uint64_t* __restrict__ keys, uint64_t W, uint64_t* __restrict__ head) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= W) return;
+  head[i] = (keys[i] != ~0ull) && (i == 0 || keys[i] != keys[i - 1]);
+}
+
+// seg = inclusive-scan(head) - 1; accumulate the item's row into its segment.
+__global__ void k_seg_accumulate(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ idx,
+                                 const uint64_t* __restrict__ segx, const uint64_t* __restrict__ head,
+                                 const uint64_t* __restrict__ rows, uint32_t P, uint64_t W,
+                                 uint64_t* __restrict__ key_out, uint64_t* __restrict__ pay_out, int* err) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= W || keys[i] == ~0ull) return;
+  const uint64_t seg = segx[i] + head[i] - 1;  // exclusive scan + own head = inclusive
+  if (head[i]) key_out[seg] = keys[i];
+  const uint64_t* row = rows + idx[i] * P;
+  for (uint32_t j = 0; j < P; ++j)
+    if (row[j]) atomic_add_ck(reinterpret_cast<u64*>(pay_out + seg * P + j), row[j], err);
+}
+
+__global__ void k_init_frontier(uint32_t x0, uint32_t nx, int bits, const uint8_t* __restrict__ chi,
+                                const uint64_t* __restrict__ utab, uint32_t Pu, uint64_t* __restrict__ key,
+                                uint64_t* __restrict__ pay) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= nx) return;
+  const uint64_t x = x0 + i;
+  key[i] = (x << bits) | x;
+  if (utab) {
+    for (uint32_t j = 0; j < Pu; ++j) pay[static_cast<uint64_t>(i) * Pu + j] = utab[x * Pu + j];
+  } else {
+    pay[i] = 1;  // signature {chi x}
+  }
+}
+
+struct MergeArgs {
+  GraphView G;
+  // side A (iterated; may carry r), side B (looked up by (x, v))
+  const uint64_t* keyA;
+  const uint64_t* payA;
+  uint64_t nA;
+  int sA;
+  uint32_t PA;
+  int A_has_r;
+  const uint64_t* keyB;
+  const uint64_t* payB;
+  uint64_t nB;
+  int sB;
+  uint32_t PB;
+  int bits;
+  // output
+  int out_kind;  // 1 scalar, 2 vertex, 3 edge, 4 pair (contribution rows)
+  uint64_t* ckey;   // pair: [nA] keys (UINT64_MAX = none)
+  uint64_t* crow;   // pair: [nA][Pout]
+  int key_src0, key_src1;  // 0 = x, 1 = v, 2 = r
+  uint64_t* out;
+  uint32_t Pout;
+  u64* scalar;
+  int* err;
+  u64* updates;
+};
+
+__device__ __forceinline__ uint64_t find_slot(const GraphView& G, uint32_t p, uint32_t q) {
+  uint64_t lo = G.off[p], hi = G.off[p + 1];
+  while (lo < hi) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (G.adj[mid] < q) lo = mid + 1; else hi = mid;
+  }
+  return (lo < G.off[p + 1] && G.adj[lo] == q) ? lo : ~0ull;
+}
+
+__global__ void __launch_bounds__(256) k_half_merge(MergeArgs A) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  uint64_t local = 0, upd = 0;
+  if (i < A.nA) {
+    uint32_t x, v, r;
+    unpack_key(A.keyA[i], A.A_has_r, A.bits, x, v, r);
+    const uint64_t kb = (static_cast<uint64_t>(x) << A.bits) | v;
+    uint64_t lo = 0, hi = A.nB;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (A.keyB[mid] < kb) lo = mid + 1; else hi = mid;
+    }
+    if (A.out_kind == 4) {
+      A.ckey[i] = ~0ull;
+      for (uint32_t j = 0; j < A.Pout; ++j) A.crow[i * A.Pout + j] = 0;
+    }
+    if (lo < A.nB && A.keyB[lo] == kb) {
+      const uint32_t cx = A.G.chi[x], cv = A.G.chi[v];
+      const uint32_t fx = 1u << cx, fv = 1u << cv, f2 = fx | fv;
+      const uint32_t ids[3] = {x, v, r};
+      uint64_t orow = 0;
+      uint32_t ofix = 0;
+      if (A.out_kind == 2) {
+        const uint32_t y = ids[A.key_src0];
+        orow = static_cast<uint64_t>(y) * A.Pout;
+        ofix = 1u << A.G.chi[y];
+      } else if (A.out_kind == 3) {
+        const uint32_t p = ids[A.key_src0], q = ids[A.key_src1];
+        const uint64_t s = find_slot(A.G, p, q);
+        if (s == ~0ull) {
+          atomicOr(A.err, 4);  // pair not adjacent: plan/table kind mismatch
+          return;
+        }
+        orow = s * A.Pout;
+        ofix = (1u << A.G.chi[p]) | (1u << A.G.chi[q]);
+      } else if (A.out_kind == 4) {
+        const uint32_t p = ids[A.key_src0], q = ids[A.key_src1];
+        A.ckey[i] = (static_cast<uint64_t>(p) << A.bits) | q;
+        orow = i * A.Pout;
+        ofix = (1u << A.G.chi[p]) | (1u << A.G.chi[q]);
+      }
+      const uint64_t* ra = A.payA + i * A.PA;
+      const uint64_t* rb = A.payB + lo * A.PB;
+      const int ta = A.sA - 2, tb = A.sB - 2;
+      for (uint32_t ia = 0; ia < A.PA; ++ia) {
+        const uint64_t va = ra[ia];
+        if (!va) continue;
+        const uint32_t Sa = sig_expand(sig_unrank(c_lut, ta, ia), f2);
+        for (uint32_t ib = 0; ib < A.PB; ++ib) {
+          const uint64_t vb = rb[ib];
+          if (!vb) continue;
+          const uint32_t Sb = sig_expand(sig_unrank(c_lut, tb, ib), f2);
+          if ((Sa & Sb) != f2) continue;
+          const uint64_t val = mul_ck(va, vb, A.err);
+          ++upd;
+          if (A.out_kind == 1) {
+            local = add_ck(local, val, A.err);
+          } else if (A.out_kind == 4) {
+            uint64_t* c = A.crow + orow + sig_index(c_lut, Sa | Sb, ofix);
+            *c = add_ck(*c, val, A.err);
+          } else {
+            atomic_add_ck(reinterpret_cast<u64*>(A.out + orow + sig_index(c_lut, Sa | Sb, ofix)), val, A.err);
+          }
+        }
+      }
+    }
+  }
+  if (A.out_kind == 1) {
+    for (int o = 16; o > 0; o >>= 1) local = add_ck(local, __shfl_down_sync(0xffffffffu, local, o), A.err);
+    if ((threadIdx.x & 31) == 0 && local) atomic_add_ck(A.scalar, local, A.err);
+  }
+  for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(0xffffffffu, upd, o);
+  if ((threadIdx.x & 31) == 0 && upd) atomicAdd(A.updates, static_cast<u64>(upd));
+}
+
+// Host side --------------------------------------------------------------------
+
+struct CycleDesc {
+  int L = 0;
+  std::vector<TabView> node, edge;  // per position / per edge (edge i: i -> i+1)
+  std::vector<char> edge_fwd;
+  std::vector<int> bpos;
+  TabView out;
+  int s_out = 0;
+};
+
+struct Frontier {
+  DBuf key, pay;
+  uint64_t n = 0;
+  int s = 0;
+  uint32_t P = 0;
+  int has_r = 0;
+};
+
+// Rows of a relation as seen when walking from the first key to the second.
+struct Relation {
+  const uint64_t* off;
+  const uint32_t* adj;
+  const uint64_t* pay = nullptr;  // per-slot payload rows (null: plain graph edges)
+  uint32_t P = 0;
+  int s = 0;
+  int use_rev = 0;                // payload row = rev[slot] (edge tables walked backwards)
+};
+
+__global__ void k_pair_csr(uint32_t n, const uint64_t* __restrict__ keys, uint64_t nk, int bits,
+                           uint64_t* __restrict__ off, uint32_t* __restrict__ cols) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i < nk) cols[i] = static_cast<uint32_t>(keys[i] & ((1ull << bits) - 1));
+  if (i <= n) {
+    const uint64_t target = i << bits;
+    uint64_t lo = 0, hi = nk;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (keys[mid] < target) lo = mid + 1; else hi = mid;
+    }
+    off[i] = lo;
+  }
+}
+
+__global__ void k_swap_pair_keys(const uint64_t* __restrict__ in, uint64_t nk, int bits, uint64_t* __restrict__ out) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= nk) return;
+  const uint64_t mask = (1ull << bits) - 1;
+  out[i] = ((in[i] & mask) << bits) | (in[i] >> bits);
+}
+
+__global__ void k_gather_rows(const uint64_t* __restrict__ idx, const uint64_t* __restrict__ in, uint32_t P,
+                              uint64_t nk, uint64_t* __restrict__ out) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= nk * P) return;
+  const uint64_t r = i / P, j = i - r * P;
+  out[i] = in[idx[r] * P + j];
+}
+
+struct PairBuild {  // merge contributions of a pair-keyed block
+  std::vector<DBuf> keys, rows;
+  std::vector<uint64_t> counts;
+};
+
+struct CycleRunner {
+  GraphView G;
+  int k = 0;
+  int bits = 0;
+  cudaStream_t stream;
+  int* err;
+  u64* scalar;
+  u64* upd;
+  std::function<void(const char*, const std::function<void()>&)> launch;
+  std::function<void(const uint64_t*, uint64_t*, uint64_t)> scan;  // exclusive scan of n+1
+  DBuf sort_tmp;
+  uint64_t mem_budget = 6ull << 30;  // bytes of per-hop scratch per batch
+  bool force = false;                 // single-anchor batch: no further split
+  PairBuild pairs;
+
+  static uint64_t binom(int a, int b) { return binom_host(a, b); }
+
+  uint64_t d2h(const uint64_t* p) {
+    uint64_t v = 0;
+    MB_CUDA(cudaMemcpyAsync(&v, p, 8, cudaMemcpyDeviceToHost, stream));
+    MB_CUDA(cudaStreamSynchronize(stream));
+    return v;
+  }
+
+  void sort_pairs(const uint64_t* kin, uint64_t* kout, const uint64_t* vin, uint64_t* vout, uint64_t W) {
+    size_t tmp = 0;
+    MB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, static_cast<int64_t>(W), 0, 64, stream));
+    if (sort_tmp.bytes < tmp) sort_tmp.alloc(tmp);
+    MB_CUDA(cub::DeviceRadixSort::SortPairs(sort_tmp.p, tmp, kin, kout, vin, vout, static_cast<int64_t>(W), 0, 64,
+                                            stream));
+  }
+
+  // Sort contributions (keys[W], rows[W][P]) and add equal keys: the
+  // reference's hash-map accumulate (table.cpp:190) as sort + segmented add.
+  // Keys equal to UINT64_MAX are dropped.
+  void aggregate(const DBuf& keys, const DBuf& rows, uint64_t W, uint32_t P, DBuf& out_key, DBuf& out_pay,
+                 uint64_t& out_n) {
+    DBuf idx(W * 8), skeys(W * 8), sidx(W * 8);
+    launch("cycle_iota", [&] { k_iota<<<grid_for(W, 256), 256, 0, stream>>>(idx.as<uint64_t>(), W); });
+    sort_pairs(keys.as<uint64_t>(), skeys.as<uint64_t>(), idx.as<uint64_t>(), sidx.as<uint64_t>(), W);
+    DBuf head((W + 1) * 8), segx((W + 1) * 8);
+    MB_CUDA(cudaMemsetAsync(head.p, 0, (W + 1) * 8, stream));
+    launch("cycle_seg_heads", [&] {
+      k_seg_heads<<<grid_for(W, 256), 256, 0, stream>>>(skeys.as<uint64_t>(), W, head.as<uint64_t>());
+    });
+    scan(head.as<uint64_t>(), segx.as<uint64_t>(), W + 1);
+    out_n = d2h(segx.as<uint64_t>() + W);
+    out_key.alloc(std::max<uint64_t>(out_n, 1) * 8);
+    out_pay.alloc(std::max<uint64_t>(out_n * P, 1) * 8);
+    MB_CUDA(cudaMemsetAsync(out_pay.p, 0, out_pay.bytes, stream));
+    if (out_n)
+      launch("cycle_seg_accumulate", [&] {
+        k_seg_accumulate<<<grid_for(W, 256), 256, 0, stream>>>(skeys.as<uint64_t>(), sidx.as<uint64_t>(),
+                                                               segx.as<uint64_t>(), head.as<uint64_t>(),
+                                                               rows.as<uint64_t>(), P, W, out_key.as<uint64_t>(),
+                                                               out_pay.as<uint64_t>(), err);
+      });
+  }
+
+  // Returns false when the hop exceeded the scratch budget (caller splits the batch).
+  bool hop(const Frontier& in, Frontier& out, const Relation& rel, const TabView& nt, bool record, bool first) {
+    out.has_r = in.has_r || record;
+    out.s = in.s + 1 + (rel.pay ? rel.s - 2 : 0) + (nt.kind ? nt.s - 1 : 0);
+    out.P = static_cast<uint32_t>(binom(k - 2, out.s - 2));
+    out.n = 0;
+    if (in.n == 0) return true;
+    DBuf work((in.n + 1) * 8), woff((in.n + 1) * 8);
+    MB_CUDA(cudaMemsetAsync(work.p, 0, (in.n + 1) * 8, stream));
+    launch("cycle_hop_work", [&] {
+      k_hop_work<<<grid_for(in.n, 256), 256, 0, stream>>>(in.key.as<uint64_t>(), in.n, in.has_r, bits, rel.off,
+                                                          work.as<uint64_t>());
+    });
+    scan(work.as<uint64_t>(), woff.as<uint64_t>(), in.n + 1);
+    const uint64_t W = d2h(woff.as<uint64_t>() + in.n);
+    if (W == 0) return true;
+    if (W * (out.P * 8ull + 72) > mem_budget && !force) return false;
+    DBuf keys(W * 8), rows(W * out.P * 8);
+    HopArgs A{};
+    A.G = G;
+    A.key_in = in.key.as<uint64_t>();
+    A.pay_in = in.pay.as<uint64_t>();
+    A.n_in = in.n;
+    A.s_in = in.s;
+    A.P_in = in.P;
+    A.first_hop = first;
+    A.in_has_r = in.has_r;
+    A.woff = woff.as<uint64_t>();
+    A.W = W;
+    A.roff = rel.off;
+    A.radj = rel.adj;
+    if (rel.pay) A.etab = rel.pay, A.Pe = rel.P, A.se = rel.s, A.e_rev = rel.use_rev;
+    if (nt.kind) A.ntab = nt.data, A.Pn = nt.P, A.sn = nt.s;
+    A.record = record;
+    A.s_out = out.s;
+    A.P_out = out.P;
+    A.out_has_r = out.has_r;
+    A.bits = bits;
+    A.key_out = keys.as<uint64_t>();
+    A.row_out = rows.as<uint64_t>();
+    A.err = err;
+    A.updates = upd;
+    launch("cycle_hop_expand", [&] { k_hop_expand<<<grid_for(W, 256), 256, 0, stream>>>(A); });
+    aggregate(keys, rows, W, out.P, out.key, out.pay, out.n);
+    return true;
+  }
+
+  // Relation for the cycle edge e walked from position p to q.
+  Relation relation(const CycleDesc& C, int e, bool walk_fwd_of_storage) const {
+    Relation r;
+    const TabView& t = C.edge[e];
+    if (t.kind == 4) {
+      r.off = walk_fwd_of_storage ? t.off : t.off_t;
+      r.adj = walk_fwd_of_storage ? t.cols : t.cols_t;
+      r.pay = walk_fwd_of_storage ? t.data : t.data_t;
+      r.P = t.P, r.s = t.s;
+    } else {
+      r.off = G.off, r.adj = G.adj;
+      if (t.kind == 3) r.pay = t.data, r.P = t.P, r.s = t.s, r.use_rev = !walk_fwd_of_storage;
+    }
+    return r;
+  }
+
+  // Builds one half path from h towards d for anchors [x0, x0 + nx).
+  bool half(const CycleDesc& C, int h, int d, bool cw, bool start_ann, bool end_ann, int rec_pos, uint32_t x0,
+            uint32_t nx, Frontier& f) {
+    const int L = C.L;
+    Frontier cur;
+    const TabView& hn = C.node[h];
+    const bool use_start = start_ann && hn.kind;
+    cur.s = use_start ? hn.s : 1;
+    cur.P = use_start ? hn.P : 1;
+    cur.n = nx;
+    cur.has_r = 0;
+    cur.key.alloc(std::max<uint32_t>(nx, 1) * 8);
+    cur.pay.alloc(std::max<uint64_t>(static_cast<uint64_t>(nx) * cur.P, 1) * 8);
+    launch("cycle_init", [&] {
+      k_init_frontier<<<grid_for(nx, 256), 256, 0, stream>>>(x0, nx, bits, G.chi, use_start ? hn.data : nullptr,
+                                                             cur.P, cur.key.as<uint64_t>(), cur.pay.as<uint64_t>());
+    });
+    int p = h;
+    bool first = true;
+    const TabView none{};
+    while (p != d) {
+      const int q = cw ? (p + 1) % L : (p + L - 1) % L;
+      const int e = cw ? p : q;  // cycle edge joining p and q
+      // child keyed (nodes[e], nodes[e+1]) when edge_fwd; we walk p -> q
+      const bool stored_pq = cw ? static_cast<bool>(C.edge_fwd[e]) : !C.edge_fwd[e];
+      const Relation rel = relation(C, e, C.edge[e].kind ? stored_pq : true);
+      const TabView& nt = (q != d || end_ann) ? C.node[q] : none;
+      Frontier nxt;
+      if (!hop(cur, nxt, rel, nt.kind ? nt : none, q == rec_pos, first)) return false;
+      cur = std::move(nxt);
+      first = false;
+      p = q;
+    }
+    f = std::move(cur);
+    return true;
+  }
+
+  // Evaluates position h of Eq. 1 for anchors [x0, x0+nx); false = split and
+  // retry (nothing has been accumulated for this (h, batch) yet).
+  bool run_batch(const CycleDesc& C, int h, uint32_t x0, uint32_t nx) {
+    const int L = C.L, nb = static_cast<int>(C.bpos.size());
+    int d, rec = -1;
+    int ks0 = 0, ks1 = 0;  // output key sources: 0 x, 1 v, 2 r
+    if (nb == 0) {
+      d = (h + L / 2) % L;
+    } else if (nb == 1) {
+      if (C.bpos[0] == h) {
+        d = (h + L / 2) % L;
+        ks0 = 0;
+      } else {
+        d = C.bpos[0];
+        ks0 = 1;
+      }
+    } else {
+      if (h == C.bpos[0]) {
+        d = C.bpos[1], ks0 = 0, ks1 = 1;
+      } else if (h == C.bpos[1]) {
+        d = C.bpos[0], ks0 = 1, ks1 = 0;
+      } else {
+        d = C.bpos[0], rec = C.bpos[1], ks0 = 1, ks1 = 2;
+      }
+    }
+    bool rec_cw = false;
+    for (int p = h; p != d; p = (p + 1) % L)
+      if (p == rec) rec_cw = true;
+    Frontier fp, fm;
+    // plus (clockwise): excludes the start annotation, includes the end (d)
+    if (!half(C, h, d, true, false, true, rec_cw ? rec : -1, x0, nx, fp)) return false;
+    // minus (counter-clockwise): includes the start annotation, excludes the end
+    if (!half(C, h, d, false, true, false, (rec >= 0 && !rec_cw) ? rec : -1, x0, nx, fm)) return false;
+    if (fp.n == 0 || fm.n == 0) return true;
+    const Frontier& A = fp.has_r ? fp : fm;
+    const Frontier& B = fp.has_r ? fm : fp;
+    MergeArgs M{};
+    M.G = G;
+    M.keyA = A.key.as<uint64_t>(), M.payA = A.pay.as<uint64_t>(), M.nA = A.n, M.sA = A.s, M.PA = A.P;
+    M.A_has_r = A.has_r;
+    M.keyB = B.key.as<uint64_t>(), M.payB = B.pay.as<uint64_t>(), M.nB = B.n, M.sB = B.s, M.PB = B.P;
+    M.bits = bits;
+    M.out_kind = C.out.kind == 1 ? 1 : (C.out.kind == 2 ? 2 : (C.out.kind == 3 ? 3 : 4));
+    M.key_src0 = ks0, M.key_src1 = ks1;
+    M.out = C.out.data, M.Pout = C.out.P;
+    M.scalar = scalar, M.err = err, M.updates = upd;
+    DBuf ck, cr;
+    if (M.out_kind == 4) {
+      ck.alloc(A.n * 8);
+      cr.alloc(std::max<uint64_t>(A.n * C.out.P, 1) * 8);
+      M.ckey = ck.as<uint64_t>(), M.crow = cr.as<uint64_t>();
+    }
+    launch("cycle_merge", [&] { k_half_merge<<<grid_for(A.n, 256), 256, 0, stream>>>(M); });
+    if (M.out_kind == 4) {
+      pairs.keys.push_back(std::move(ck));
+      pairs.rows.push_back(std::move(cr));
+      pairs.counts.push_back(A.n);
+    }
+    return true;
+  }
+
+  void solve(const CycleDesc& C) {
+    const uint32_t first_batch = std::max<uint32_t>(1, std::min<uint32_t>(G.n, 1u << 20));
+    for (int h = 0; h < C.L; ++h) {
+      std::vector<std::pair<uint32_t, uint32_t>> todo;
+      for (uint32_t x = 0; x < G.n; x += first_batch) todo.push_back({x, std::min(first_batch, G.n - x)});
+      std::reverse(todo.begin(), todo.end());
+      while (!todo.empty()) {
+        const auto [x0, nx] = todo.back();
+        todo.pop_back();
+        force = nx == 1;
+        if (run_batch(C, h, x0, nx)) continue;
+        const uint32_t a = nx / 2;
+        todo.push_back({x0 + a, nx - a});
+        todo.push_back({x0, a});
+      }
+    }
+  }
+
+  // Concatenates the pair contributions of solve() and aggregates them into a
+  // sorted pair table with CSR rows (and the transposed copy).
+  void finish_pairs(uint32_t P, DBuf& key, DBuf& pay, uint64_t& nk, DBuf& off, DBuf& cols, DBuf& off_t,
+                    DBuf& cols_t, DBuf& pay_t) {
+    uint64_t W = 0;
+    for (uint64_t c : pairs.counts) W += c;
+    nk = 0;
+    if (W) {
+      DBuf allk(W * 8), allr(W * P * 8);
+      uint64_t o = 0;
+      for (size_t i = 0; i < pairs.counts.size(); ++i) {
+        const uint64_t c = pairs.counts[i];
+        MB_CUDA(cudaMemcpyAsync(allk.as<uint64_t>() + o, pairs.keys[i].p, c * 8, cudaMemcpyDeviceToDevice, stream));
+        MB_CUDA(cudaMemcpyAsync(allr.as<uint64_t>() + o * P, pairs.rows[i].p, c * P * 8, cudaMemcpyDeviceToDevice,
+                                stream));
+        o += c;
+      }
+      pairs = PairBuild{};
+      aggregate(allk, allr, W, P, key, pay, nk);
+    } else {
+      key.alloc(8);
+      pay.alloc(8);
+    }
+    build_csr(key, nk, off, cols);
+    // transpose: swap the two keys, sort, gather rows
+    DBuf tk(std::max<uint64_t>(nk, 1) * 8), idx(std::max<uint64_t>(nk, 1) * 8), sk(std::max<uint64_t>(nk, 1) * 8),
+        sidx(std::max<uint64_t>(nk, 1) * 8);
+    pay_t.alloc(std::max<uint64_t>(nk * P, 1) * 8);
+    if (nk) {
+      launch("pair_swap", [&] { k_swap_pair_keys<<<grid_for(nk, 256), 256, 0, stream>>>(key.as<uint64_t>(), nk, bits, tk.as<uint64_t>()); });
+      launch("cycle_iota", [&] { k_iota<<<grid_for(nk, 256), 256, 0, stream>>>(idx.as<uint64_t>(), nk); });
+      sort_pairs(tk.as<uint64_t>(), sk.as<uint64_t>(), idx.as<uint64_t>(), sidx.as<uint64_t>(), nk);
+      launch("pair_gather", [&] {
+        k_gather_rows<<<grid_for(nk * P, 256), 256, 0, stream>>>(sidx.as<uint64_t>(), pay.as<uint64_t>(), P, nk,
+                                                                 pay_t.as<uint64_t>());
+      });
+    }
+    build_csr(sk, nk, off_t, cols_t);
+  }
+
+  void build_csr(const DBuf& keys, uint64_t nk, DBuf& off, DBuf& cols) {
+    off.alloc((static_cast<uint64_t>(G.n) + 1) * 8);
+    cols.alloc(std::max<uint64_t>(nk, 1) * 4);
+    launch("pair_csr", [&] {
+      k_pair_csr<<<grid_for(std::max<uint64_t>(nk, static_cast<uint64_t>(G.n) + 1), 256), 256, 0, stream>>>(
+          G.n, keys.as<uint64_t>(), nk, bits, off.as<uint64_t>(), cols.as<uint32_t>());
+    });
+  }
+};

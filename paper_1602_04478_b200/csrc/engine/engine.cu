@@ -4,7 +4,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cstdlib>
+#include <functional>
 #include <map>
 #include <numeric>
 #include <string>
@@ -212,7 +215,7 @@ __global__ void k_triangles(uint32_t n, uint64_t nout, const uint64_t* __restric
 // ------------------------------------------------------------- leaf blocks
 
 struct LeafArgs {
-  const uint64_t* off;
+  const uint64_t* off;   // relation rows (graph CSR or a pair table's CSR)
   const uint32_t* adj;
   const uint32_t* rev;
   const uint8_t* chi;
@@ -455,18 +458,22 @@ unsigned grid_for(uint64_t work, unsigned block) {
   return static_cast<unsigned>(std::max<uint64_t>(1, g));
 }
 
+#include "cycle_engine.cuh"
+
 }  // namespace
 
 // ---------------------------------------------------------------- the engine
 
-enum class TKind { None, Scalar, Vertex, Edge };
+enum class TKind { None, Scalar, Vertex, Edge, Pair };
 
 struct DevTable {
   TKind kind = TKind::None;
   int s = 0;
   uint32_t P = 0;
-  uint64_t rows = 0;
-  DBuf buf;
+  uint64_t rows = 0;  // Vertex: n, Edge: 2m, Pair: number of pairs
+  DBuf buf;           // payload rows
+  // Pair tables: sorted packed keys, CSR by first key, transposed copy
+  DBuf keys, off, cols, off_t, cols_t, buf_t;
   uint64_t* data() const { return buf.as<uint64_t>(); }
 };
 
@@ -478,6 +485,7 @@ struct StepPlan {
   std::vector<char> edge_fwd;
   std::vector<int> bpos;
   int s_out = 0;
+  bool general = false;  // cycle solved by the general half-path engine
 };
 
 struct GpuEngine::Impl {
@@ -663,7 +671,6 @@ struct GpuEngine::Impl {
       for (int x : b.boundary) sp.bpos.push_back(b.pos(x));
       DevTable& out = tables[id];
       out.s = sp.s_out;
-      const bool is_root = id == p.root;
       if (b.kind == BlockKind::Leaf || b.boundary.size() == 1) {
         out.kind = TKind::Vertex;
         out.P = static_cast<uint32_t>(binom(k - 1, sp.s_out - 1));
@@ -672,28 +679,26 @@ struct GpuEngine::Impl {
         out.kind = TKind::Scalar;
       } else {
         // two boundary nodes: stored per CSR slot when the pair is always a
-        // graph edge (cycle-adjacent through an original or edge-keyed edge)
+        // graph edge (cycle-adjacent through an original or edge-keyed edge),
+        // otherwise as a sorted pair table
         const int d = (sp.bpos[1] - sp.bpos[0] + sp.L) % sp.L;
         int e = -1;
         if (d == 1) e = sp.bpos[0];
         if (d == sp.L - 1) e = sp.bpos[1];
-        const bool supported = e >= 0 && (sp.edge_tab[e] < 0 || tables[sp.edge_tab[e]].kind == TKind::Edge);
-        if (!supported)
-          fail(kSpec, "plan needs a projection table over non-adjacent vertex pairs (block " + b.canonical() +
-                          "); not yet supported by the GPU engine");
-        out.kind = TKind::Edge;
+        const bool on_edges = e >= 0 && (sp.edge_tab[e] < 0 || tables[sp.edge_tab[e]].kind == TKind::Edge);
+        out.kind = on_edges ? TKind::Edge : TKind::Pair;
         out.P = static_cast<uint32_t>(binom(k - 2, sp.s_out - 2));
-        out.rows = m2;
+        out.rows = on_edges ? m2 : 0;
       }
-      (void)is_root;
       if (b.kind == BlockKind::Cycle) {
+        bool edge_children_on_edges = true;
         for (int e = 0; e < sp.L; ++e)
-          if (sp.edge_tab[e] >= 0 && tables[sp.edge_tab[e]].kind != TKind::Edge)
-            fail(kSpec, "cycle edge annotated with a non-edge table; not yet supported");
-        if (sp.L == 3) needs_triangles = true;
-        else fail(kSpec, "cycle blocks longer than 3 are not yet supported by the GPU engine");
-      } else if (sp.edge_tab[0] >= 0 && tables[sp.edge_tab[0]].kind != TKind::Edge) {
-        fail(kSpec, "leaf edge annotated with a non-edge table; not yet supported");
+          if (sp.edge_tab[e] >= 0 && tables[sp.edge_tab[e]].kind != TKind::Edge) edge_children_on_edges = false;
+        static const bool force_general = std::getenv("MB_FORCE_GENERAL_CYCLES") != nullptr;
+        if (sp.L == 3 && edge_children_on_edges && out.kind != TKind::Pair && !force_general)
+          needs_triangles = true;
+        else
+          sp.general = true;
       }
       if (out.kind == TKind::Vertex || out.kind == TKind::Edge) {
         out.buf.alloc(std::max<uint64_t>(out.rows * out.P, 1) * sizeof(uint64_t));
@@ -718,7 +723,18 @@ struct GpuEngine::Impl {
     int s_right = 2;
     if (sp.edge_tab[0] >= 0) {
       const DevTable& t = tables[sp.edge_tab[0]];
-      A.ue = t.data(), A.Pe = t.P, A.se = t.s, A.e_rev = !sp.edge_fwd[0];
+      if (t.kind == TKind::Pair) {
+        // rows keyed by the boundary image: the stored table when the child is
+        // keyed (a, b), its transpose otherwise
+        const bool fwd = sp.edge_fwd[0];
+        A.off = (fwd ? t.off : t.off_t).as<uint64_t>();
+        A.adj = (fwd ? t.cols : t.cols_t).as<uint32_t>();
+        A.ue = (fwd ? t.buf : t.buf_t).as<uint64_t>();
+        A.e_rev = 0;
+      } else {
+        A.ue = t.data(), A.e_rev = !sp.edge_fwd[0];
+      }
+      A.Pe = t.P, A.se = t.s;
       s_right = t.s;
     }
     if (sp.node_tab[1] >= 0) {
@@ -799,6 +815,55 @@ struct GpuEngine::Impl {
       launch("triangle_block", [&] { triangle_block_kernel<<<grid_for(ntri * 6, 256), 256, 0, stream>>>(A); });
   }
 
+  TabView view(int tab) const {
+    TabView v;
+    if (tab < 0) return v;
+    const DevTable& t = tables[tab];
+    v.kind = t.kind == TKind::Scalar ? 1 : t.kind == TKind::Vertex ? 2 : t.kind == TKind::Edge ? 3
+           : t.kind == TKind::Pair ? 4 : 0;
+    v.s = t.s;
+    v.P = t.P;
+    v.data = t.data();
+    if (t.kind == TKind::Pair) {
+      v.off = t.off.as<uint64_t>(), v.cols = t.cols.as<uint32_t>();
+      v.off_t = t.off_t.as<uint64_t>(), v.cols_t = t.cols_t.as<uint32_t>();
+      v.data_t = t.buf_t.as<uint64_t>();
+    }
+    return v;
+  }
+
+  void run_general(const StepPlan& sp, int* err, u64* scalar, u64* upd) {
+    CycleDesc C;
+    C.L = sp.L;
+    for (int q = 0; q < sp.L; ++q) C.node.push_back(view(sp.node_tab[q]));
+    for (int e = 0; e < sp.L; ++e) C.edge.push_back(view(sp.edge_tab[e]));
+    C.edge_fwd = sp.edge_fwd;
+    C.bpos = sp.bpos;
+    C.out = view(sp.block);
+    C.s_out = sp.s_out;
+    CycleRunner R;
+    R.G = GraphView{n, m2, off.as<uint64_t>(), adj.as<uint32_t>(), rev.as<uint32_t>(), rank.as<uint32_t>(),
+                    chi.as<uint8_t>()};
+    R.k = k;
+    int bits = 1;
+    while (bits < 32 && (1ull << bits) < n) ++bits;
+    R.bits = bits;
+    const bool rec = sp.bpos.size() == 2;
+    if ((rec ? 3 : 2) * bits > 64)
+      fail(kSpec, "graph too large for the general cycle engine's packed keys");
+    R.stream = stream;
+    R.err = err;
+    R.scalar = scalar;
+    R.upd = upd;
+    R.launch = [this](const char* name, const std::function<void()>& f) { launch(name, f); };
+    R.scan = [this](const uint64_t* in, uint64_t* o, uint64_t c) { exclusive_scan(in, o, c); };
+    R.solve(C);
+    DevTable& out = tables[sp.block];
+    if (out.kind == TKind::Pair) {
+      R.finish_pairs(out.P, out.keys, out.buf, out.rows, out.off, out.cols, out.off_t, out.cols_t, out.buf_t);
+    }
+  }
+
   void count(const uint8_t* chi_src, int nc, bool host, uint64_t* result) {
     if (!plan_bound) fail(kSpec, "no plan bound");
     if (k == 1) {
@@ -828,6 +893,7 @@ struct GpuEngine::Impl {
         if (out.kind == TKind::Edge || (out.kind == TKind::Vertex && sp.kind == BlockKind::Cycle))
           MB_CUDA(cudaMemsetAsync(out.buf.p, 0, out.buf.bytes, stream));
         if (sp.kind == BlockKind::Leaf) run_leaf(sp, err, upd);
+        else if (sp.general) run_general(sp, err, scalar, upd);
         else run_triangle(sp, err, scalar, upd);
       }
       if (plan.singleton_root) {
@@ -844,6 +910,7 @@ struct GpuEngine::Impl {
     for (int c = 0; c < nc; ++c) {
       const int e = static_cast<int>(host_flags[3 * c] & 0xffffffffu);
       if (e & 2) fail(kSpec, "colouring has a colour outside 1..k");
+      if (e & 4) fail(kInternal, "edge-keyed output received a non-adjacent vertex pair");
       if (e & 1) fail(kOverflow, "count overflow (64-bit)");
       result[c] = host_flags[3 * c + 1];
       st.dp_updates += host_flags[3 * c + 2];

@@ -57,3 +57,54 @@ def test_every_tree_same_count(mb, reference):
     for t in range(plan.num_trees()):
         plan.use_tree(t)
         assert mb.count_colorful(g, plan, chi) == want, plan.canonical(t)
+
+
+CYCLE_FAMILY = {
+    "c4": (4, [(0, 1), (1, 2), (2, 3), (3, 0)]),
+    "c5": (5, [(0, 1), (1, 2), (2, 3), (3, 4), (4, 0)]),
+    "c6": (6, [(i, (i + 1) % 6) for i in range(6)]),
+    "c7": (7, [(i, (i + 1) % 7) for i in range(7)]),
+    "c5_pendant": (6, [(0, 1), (1, 2), (2, 3), (3, 4), (4, 0), (2, 5)]),
+    "theta": (8, [(0, 1), (1, 2), (2, 7), (0, 3), (3, 4), (4, 7), (0, 5), (5, 6), (6, 7)]),
+    "sp10": (10, [(0, 1), (1, 2), (2, 3), (3, 4), (4, 5), (5, 0), (0, 2), (3, 5), (1, 6), (6, 7), (7, 8),
+                  (8, 9), (9, 1)]),
+    "brain1": (9, [(0, 1), (1, 2), (2, 3), (3, 0), (0, 4), (4, 5), (5, 6), (6, 7), (7, 8), (8, 0)]),
+    "sat": (11, [(0, 1), (1, 2), (2, 3), (3, 4), (4, 0), (0, 5), (2, 6), (5, 6), (5, 7), (5, 8), (6, 8),
+                 (8, 9), (9, 10), (10, 8)]),
+    "k4_minus": (4, [(0, 1), (1, 2), (2, 3), (3, 0), (0, 2)]),
+}
+
+
+@pytest.mark.parametrize("name", sorted(CYCLE_FAMILY))
+def test_cycles_against_brute_force(mb, oracle, name):
+    k, q = CYCLE_FAMILY[name]
+    plan = mb.QueryPlan(k, q)
+    n = 12 if k <= 8 else 14
+    for gseed in range(2):
+        g = mb.DataGraph.erdos_renyi(n, 3 * n, seed=100 + gseed)
+        off, adj = g.csr()
+        for cseed in range(2):
+            chi = mb.random_coloring(g, k, 7 * gseed + cseed)
+            assert mb.count_colorful(g, plan, chi) == oracle.brute(off, adj, k, q, chi), (gseed, cseed)
+
+
+@pytest.mark.parametrize("name", sorted(CYCLE_FAMILY))
+def test_cycles_against_reference_engine(mb, reference, name):
+    k, q = CYCLE_FAMILY[name]
+    plan = mb.QueryPlan(k, q)
+    g = mb.DataGraph.chung_lu(400 if k >= 8 else 1500, 2.1, 8.0, seed=21)
+    for s in (100, 101):
+        chi = mb.random_coloring(g, k, s)
+        assert mb.count_colorful(g, plan, chi) == _ref_count(reference, g, k, q, chi)
+
+
+@pytest.mark.parametrize("name", ["sat", "sp10", "theta", "brain1"])
+def test_cycle_plans_every_tree(mb, reference, name):
+    k, q = CYCLE_FAMILY[name]
+    plan = mb.QueryPlan(k, q)
+    g = mb.DataGraph.chung_lu(300, 2.1, 7.0, seed=3)
+    chi = mb.random_coloring(g, k, 9)
+    want = _ref_count(reference, g, k, q, chi)
+    for t in range(plan.num_trees()):
+        plan.use_tree(t)
+        assert mb.count_colorful(g, plan, chi) == want, plan.canonical(t)
