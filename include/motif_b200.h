@@ -121,10 +121,14 @@ int mb_partition_owner(uint32_t n, int p, uint32_t v, int* owner);
 /* ---- device engine introspection (benchmark / roofline) -------------------- */
 
 int mb_engine_enable_timing(mb_graph* g, int on);
-/* Per-kernel-name device time (ms, summed), launches and name of entry idx;
- * returns 8 when idx is past the end. */
+/* Per-kernel-name device time (ms, summed), launches, compulsory HBM bytes
+ * (summed) and name of entry idx; returns 8 when idx is past the end. */
 int mb_engine_kernel_timing(mb_graph* g, int idx, char* name, int len, double* ms,
-                            uint64_t* launches);
+                            uint64_t* launches, uint64_t* bytes);
+/* cudaStream_t the engine launches on (for CUDA-event timing by callers). */
+void* mb_engine_stream(mb_graph* g);
+/* Milliseconds spent building plan-derived graph indexes (triangle lists). */
+double mb_engine_prep_ms(mb_graph* g);
 uint64_t mb_engine_launches(mb_graph* g);
 int mb_engine_stats(mb_graph* g, uint64_t* triangles, uint64_t* table_bytes,
                     uint64_t* dp_updates);

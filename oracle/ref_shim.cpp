@@ -15,7 +15,10 @@
 //   brute_colorful               include/motif/oracle.hpp:195
 //   estimate                     include/motif/estimate.hpp:34
 // Nothing here re-implements the algorithm; it only marshals plain arrays.
+#include <atomic>
 #include <cstdint>
+#include <mutex>
+#include <thread>
 #include <cstring>
 #include <exception>
 #include <memory>
@@ -160,6 +163,43 @@ int ref_count_colorful(void* gp, const uint8_t* chi, int k, void* pp, int tree_i
                                    motif::Partition(rg->g.num_vertices(), workers));
     }
   });
+}
+
+// count_colorful for `nc` colourings (n bytes each) on up to `threads` host
+// threads, one colouring per thread at a time (the reference's estimate()
+// parallelises the same way, estimate.cpp:149).  Returns the first error.
+int ref_count_batch(void* gp, const uint8_t* chis, int nc, int k, void* pp, int engine, int threads,
+                    uint64_t* out) {
+  auto* rg = static_cast<RefGraph*>(gp);
+  auto* p = static_cast<RefPlan*>(pp);
+  const uint32_t n = rg->g.num_vertices();
+  std::atomic<int> next{0}, rc{0};
+  std::string err;
+  std::mutex mu;
+  auto worker = [&] {
+    for (;;) {
+      const int c = next.fetch_add(1);
+      if (c >= nc) return;
+      try {
+        motif::Coloring col;
+        col.k = k;
+        col.chi.assign(chis + static_cast<size_t>(c) * n, chis + static_cast<size_t>(c + 1) * n);
+        out[c] = motif::count_colorful(rg->g, col, rg->ord, p->trees[p->selected],
+                                       engine == 0 ? motif::EngineKind::PS : motif::EngineKind::DB);
+      } catch (const std::exception& e) {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!rc) {
+          rc = classify(e);
+          err = g_err;
+        }
+      }
+    }
+  };
+  std::vector<std::thread> ts;
+  for (int t = 0; t < std::max(1, std::min(threads, nc)); ++t) ts.emplace_back(worker);
+  for (auto& t : ts) t.join();
+  if (rc) g_err = err;
+  return rc;
 }
 
 // JoinStats::ops of the serial engine (the reference's load metric).

@@ -135,7 +135,10 @@ def _load() -> C.CDLL:
         "mb_partition_block": (C.c_int, [C.c_uint32, C.c_int, C.c_int, u32p, u32p]),
         "mb_partition_owner": (C.c_int, [C.c_uint32, C.c_int, C.c_uint32, C.POINTER(C.c_int)]),
         "mb_engine_enable_timing": (C.c_int, [P, C.c_int]),
-        "mb_engine_kernel_timing": (C.c_int, [P, C.c_int, C.c_char_p, C.c_int, C.POINTER(C.c_double), u64p]),
+        "mb_engine_kernel_timing": (C.c_int, [P, C.c_int, C.c_char_p, C.c_int, C.POINTER(C.c_double), u64p,
+                                              u64p]),
+        "mb_engine_stream": (C.c_void_p, [P]),
+        "mb_engine_prep_ms": (C.c_double, [P]),
         "mb_engine_launches": (C.c_uint64, [P]),
         "mb_engine_stats": (C.c_int, [P, u64p, u64p, u64p]),
         "mb_engine_reset_derived": (C.c_int, [P]),
@@ -414,17 +417,38 @@ class Partition:
         return o.value
 
 
-def engine_timings(g: DataGraph) -> list[tuple[str, float, int]]:
+def engine_timings(g: DataGraph) -> list[tuple[str, float, int, int]]:
+    """(kernel name, summed device ms, launches, summed compulsory bytes)."""
     out = []
     i = 0
     buf = C.create_string_buffer(128)
     while True:
-        ms, n = C.c_double(), C.c_uint64()
-        if lib.mb_engine_kernel_timing(g.handle, i, buf, 128, C.byref(ms), C.byref(n)) != 0:
+        ms, n, b = C.c_double(), C.c_uint64(), C.c_uint64()
+        if lib.mb_engine_kernel_timing(g.handle, i, buf, 128, C.byref(ms), C.byref(n), C.byref(b)) != 0:
             break
-        out.append((buf.value.decode(), ms.value, n.value))
+        out.append((buf.value.decode(), ms.value, n.value, b.value))
         i += 1
     return out
+
+
+def engine_enable_timing(g: DataGraph, on: bool = True) -> None:
+    _check(lib.mb_engine_enable_timing(g.handle, 1 if on else 0))
+
+
+def engine_stream(g: DataGraph) -> int:
+    return lib.mb_engine_stream(g.handle) or 0
+
+
+def engine_launches(g: DataGraph) -> int:
+    return lib.mb_engine_launches(g.handle)
+
+
+def engine_prep_ms(g: DataGraph) -> float:
+    return lib.mb_engine_prep_ms(g.handle)
+
+
+def engine_reset_derived(g: DataGraph) -> None:
+    _check(lib.mb_engine_reset_derived(g.handle))
 
 
 def engine_stats(g: DataGraph) -> dict:

@@ -327,7 +327,8 @@ int mb_engine_enable_timing(mb_graph* g, int on) {
   });
 }
 
-int mb_engine_kernel_timing(mb_graph* g, int idx, char* name, int len, double* ms, uint64_t* launches) {
+int mb_engine_kernel_timing(mb_graph* g, int idx, char* name, int len, double* ms, uint64_t* launches,
+                            uint64_t* bytes) {
   return guarded([&] {
     if (!g->eng) mb::fail(mb::kSpec, "no engine");
     const auto t = g->eng->kernel_timings();
@@ -335,8 +336,13 @@ int mb_engine_kernel_timing(mb_graph* g, int idx, char* name, int len, double* m
     std::snprintf(name, len, "%s", t[idx].name.c_str());
     *ms = t[idx].ms;
     *launches = t[idx].launches;
+    *bytes = t[idx].bytes;
   });
 }
+
+void* mb_engine_stream(mb_graph* g) { return g->eng ? g->eng->stream() : nullptr; }
+
+double mb_engine_prep_ms(mb_graph* g) { return g->eng ? g->eng->stats().prep_ms : 0.0; }
 
 uint64_t mb_engine_launches(mb_graph* g) { return g->eng ? g->eng->launches() : 0; }
 

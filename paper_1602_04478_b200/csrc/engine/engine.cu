@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cstdlib>
@@ -180,38 +181,6 @@ __global__ void k_out_fill(uint32_t n, const uint64_t* __restrict__ off, const u
   }
 }
 
-// One thread per oriented edge x->y (position j in out(x)): merge out(x) and
-// out(y); every common z closes the triangle x > y > z.  PASS 0 counts, PASS 1
-// writes {x, y, z, slot(x->y), slot(x->z), slot(y->z)}.
-template <int PASS>
-__global__ void k_triangles(uint32_t n, uint64_t nout, const uint64_t* __restrict__ out_off,
-                            const uint32_t* __restrict__ out_nbr, const uint32_t* __restrict__ out_slot,
-                            const uint32_t* __restrict__ out_src, uint64_t* __restrict__ cnt,
-                            const uint64_t* __restrict__ tri_off, uint32_t* __restrict__ tri) {
-  const uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (j >= nout) return;
-  const uint32_t x = out_src[j], y = out_nbr[j];
-  uint64_t a = out_off[x], ae = out_off[x + 1], b = out_off[y], be = out_off[y + 1];
-  uint64_t c = 0, w = PASS ? tri_off[j] : 0;
-  while (a < ae && b < be) {
-    const uint32_t za = out_nbr[a], zb = out_nbr[b];
-    if (za < zb) {
-      ++a;
-    } else if (zb < za) {
-      ++b;
-    } else {
-      if (PASS) {
-        uint32_t* t = tri + 6 * w;
-        t[0] = x, t[1] = y, t[2] = za;
-        t[3] = out_slot[j], t[4] = out_slot[a], t[5] = out_slot[b];
-        ++w;
-      }
-      ++c, ++a, ++b;
-    }
-  }
-  if (!PASS) cnt[j] = c;
-}
-
 // ------------------------------------------------------------- leaf blocks
 
 struct LeafArgs {
@@ -311,138 +280,6 @@ leaf_extend_kernel(LeafArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
   if (upd) atomicAdd(A.updates, static_cast<u64>(upd));
 }
 
-// ----------------------------------------------------------- 3-cycle blocks
-
-struct Factor {
-  const uint64_t* tab;
-  uint32_t P;
-  int s;
-  int pos_a, pos_b;  // node factor: pos_b = -1; edge factor keyed (pos_a, pos_b)
-};
-
-struct TriArgs {
-  const uint32_t* tri;  // [ntri][6]
-  uint64_t ntri;
-  const uint32_t* rev;
-  const uint8_t* chi;
-  Factor f[6];
-  int nf;
-  int out_kind;  // 0 scalar, 1 unary, 2 edge
-  int b0, b1;    // boundary positions
-  uint64_t* out;
-  uint32_t Pout;
-  u64* scalar;
-  int* err;
-  u64* updates;
-};
-
-__constant__ uint8_t c_perm[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
-
-// All labelled matches of a 3-cycle block whose three images are a
-// degree-ordered triangle x > y > z (paper Eq. 1 with h = the position of x):
-// one thread per (triangle, position assignment).  Node and edge annotations
-// are folded in with the disjoint-union join (S1 n S2 = shared key colours),
-// and the result is accumulated into the block's scalar, unary or edge table.
-__global__ void __launch_bounds__(256) triangle_block_kernel(TriArgs A) {
-  const uint64_t w = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  uint64_t local = 0, upd = 0;
-  if (w < A.ntri * 6) {
-    const uint64_t t = w / 6;
-    const int p = static_cast<int>(w - t * 6);
-    const uint32_t* T = A.tri + 6 * t;
-    const uint32_t vtx[3] = {T[0], T[1], T[2]};
-    const uint32_t col[3] = {A.chi[vtx[0]], A.chi[vtx[1]], A.chi[vtx[2]]};
-    if (col[0] != col[1] && col[0] != col[2] && col[1] != col[2]) {
-      int sv[3];  // triangle vertex (0..2) at each cycle position
-      for (int q = 0; q < 3; ++q) sv[q] = c_perm[p][q];
-      auto slot = [&](int a, int b) -> uint64_t {  // a, b triangle vertex indices
-        if (a == 0 && b == 1) return T[3];
-        if (a == 1 && b == 0) return __ldg(A.rev + T[3]);
-        if (a == 0 && b == 2) return T[4];
-        if (a == 2 && b == 0) return __ldg(A.rev + T[4]);
-        if (a == 1 && b == 2) return T[5];
-        return __ldg(A.rev + T[5]);
-      };
-      const uint64_t* row[6];
-      uint32_t fixed[6];
-      bool dead = false;
-      for (int i = 0; i < A.nf; ++i) {
-        const Factor& F = A.f[i];
-        if (F.pos_b < 0) {
-          const int a = sv[F.pos_a];
-          row[i] = F.tab + static_cast<uint64_t>(vtx[a]) * F.P;
-          fixed[i] = 1u << col[a];
-        } else {
-          const int a = sv[F.pos_a], b = sv[F.pos_b];
-          row[i] = F.tab + slot(a, b) * F.P;
-          fixed[i] = (1u << col[a]) | (1u << col[b]);
-        }
-      }
-      // Depth-first over the factors' colour sets with pruning.
-      uint32_t idx[6], mstk[7];
-      uint64_t vstk[7];
-      mstk[0] = (1u << col[0]) | (1u << col[1]) | (1u << col[2]);
-      vstk[0] = 1;
-      int d = 0;
-      if (A.nf > 0) idx[0] = 0;
-      while (!dead) {
-        if (d == A.nf) {
-          const uint32_t M = mstk[d];
-          const uint64_t V = vstk[d];
-          ++upd;
-          if (A.out_kind == 0) {
-            local = add_ck(local, V, A.err);
-          } else if (A.out_kind == 1) {
-            const int a = sv[A.b0];
-            atomic_add_ck(reinterpret_cast<u64*>(A.out) + static_cast<uint64_t>(vtx[a]) * A.Pout +
-                              sig_index(c_lut, M, 1u << col[a]),
-                          V, A.err);
-          } else {
-            const int a = sv[A.b0], b = sv[A.b1];
-            atomic_add_ck(reinterpret_cast<u64*>(A.out) + slot(a, b) * A.Pout +
-                              sig_index(c_lut, M, (1u << col[a]) | (1u << col[b])),
-                          V, A.err);
-          }
-          if (d == 0) break;
-          --d;
-          ++idx[d];
-          continue;
-        }
-        const Factor& F = A.f[d];
-        if (idx[d] >= F.P) {
-          if (d == 0) break;
-          --d;
-          ++idx[d];
-          continue;
-        }
-        const uint64_t v = __ldg(row[d] + idx[d]);
-        if (v) {
-          const int f = mb_popc(fixed[d]);
-          const uint32_t Mf = sig_expand(sig_unrank(c_lut, F.s - f, idx[d]), fixed[d]);
-          if ((Mf & mstk[d]) == fixed[d]) {
-            mstk[d + 1] = mstk[d] | Mf;
-            vstk[d + 1] = mul_ck(vstk[d], v, A.err);
-            ++d;
-            if (d < A.nf) idx[d] = 0;
-            continue;
-          }
-        }
-        ++idx[d];
-      }
-    }
-  }
-  if (A.out_kind == 0) {
-    // warp reduce with overflow detection, one atomic per warp
-    for (int o = 16; o > 0; o >>= 1) {
-      const uint64_t other = __shfl_down_sync(0xffffffffu, local, o);
-      local = add_ck(local, other, A.err);
-    }
-    if ((threadIdx.x & 31) == 0 && local) atomic_add_ck(A.scalar, local, A.err);
-  }
-  for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(0xffffffffu, upd, o);
-  if ((threadIdx.x & 31) == 0 && upd) atomicAdd(A.updates, static_cast<u64>(upd));
-}
-
 // Total of a table (singleton-root plans, reference engine.cpp:398).
 __global__ void k_table_total(const uint64_t* __restrict__ t, uint64_t count, u64* out, int* err) {
   uint64_t local = 0;
@@ -459,6 +296,8 @@ unsigned grid_for(uint64_t work, unsigned block) {
 }
 
 #include "cycle_engine.cuh"
+#include "leaf.cuh"
+#include "tri_edge.cuh"
 
 }  // namespace
 
@@ -495,10 +334,11 @@ struct GpuEngine::Impl {
   uint64_t m2 = 0;
   DBuf off, adj, rank, src, rev, vlight, vheavy;
   uint32_t nlight = 0, nheavy = 0;
+  uint64_t slots_light = 0;  // CSR slots owned by light vertices
   // derived: degree-ordered triangle list
   bool tri_ready = false;
-  uint64_t ntri = 0;
-  DBuf tri;
+  uint64_t ntri = 0, ncn = 0, nout = 0;
+  DBuf out_nbr, out_slot, out_src, cn_off, cn;  // oriented edges + their CN lists
   // plan
   bool plan_bound = false;
   int k = 0;
@@ -515,6 +355,7 @@ struct GpuEngine::Impl {
   std::map<std::string, KernelTiming> timings;
   uint64_t launch_count = 0;
   std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  std::vector<uint64_t> pending_bytes;
   std::vector<cudaEvent_t> event_pool;
 
   cudaEvent_t get_event() {
@@ -528,8 +369,11 @@ struct GpuEngine::Impl {
     return e;
   }
 
+  // Launch wrapper: error check, launch count, optional CUDA-event timing on
+  // the engine stream.  `bytes` = the kernel's compulsory (algorithmic) HBM
+  // bytes for this launch, used for the roofline.
   template <class F>
-  void launch(const char* name, F&& f) {
+  void launch(const char* name, F&& f, uint64_t bytes = 0) {
     cudaEvent_t a = nullptr, b = nullptr;
     if (timing) {
       a = get_event();
@@ -542,21 +386,25 @@ struct GpuEngine::Impl {
     if (timing) {
       MB_CUDA(cudaEventRecord(b, stream));
       pending.push_back({name, {a, b}});
+      pending_bytes.push_back(bytes);
     }
   }
 
   void collect_timings() {
-    for (auto& p : pending) {
+    for (size_t i = 0; i < pending.size(); ++i) {
+      auto& p = pending[i];
       float ms = 0;
       MB_CUDA(cudaEventElapsedTime(&ms, p.second.first, p.second.second));
       auto& t = timings[p.first];
       t.name = p.first;
       t.ms += ms;
+      t.bytes += pending_bytes[i];
       t.launches++;
       event_pool.push_back(p.second.first);
       event_pool.push_back(p.second.second);
     }
     pending.clear();
+    pending_bytes.clear();
   }
 
   void upload(const CsrGraph& g) {
@@ -585,6 +433,8 @@ struct GpuEngine::Impl {
     for (uint32_t v = 0; v < n; ++v) (g.degree(v) > 256 ? heavy : light).push_back(v);
     nlight = static_cast<uint32_t>(light.size());
     nheavy = static_cast<uint32_t>(heavy.size());
+    slots_light = 0;
+    for (uint32_t v : light) slots_light += g.degree(v);
     vlight.alloc(std::max<size_t>(light.size(), 1) * 4);
     vheavy.alloc(std::max<size_t>(heavy.size(), 1) * 4);
     if (nlight) MB_CUDA(cudaMemcpyAsync(vlight.p, light.data(), light.size() * 4, cudaMemcpyHostToDevice, stream));
@@ -595,6 +445,7 @@ struct GpuEngine::Impl {
 
   void build_triangles() {
     if (tri_ready) return;
+    const auto t0 = std::chrono::steady_clock::now();
     DBuf outdeg((n + 1) * sizeof(uint64_t)), out_off((n + 1) * sizeof(uint64_t));
     MB_CUDA(cudaMemsetAsync(outdeg.p, 0, (n + 1) * sizeof(uint64_t), stream));
     launch("tri_outdeg", [&] {
@@ -614,27 +465,40 @@ struct GpuEngine::Impl {
     });
     // out_src[j] = src[out_slot[j]]
     gather_src(out_slot.as<uint32_t>(), out_src.as<uint32_t>(), nout);
-    DBuf cnt((nout + 1) * 8), toff((nout + 1) * 8);
+    // per-oriented-edge common-neighbour lists: count, scan, fill
+    DBuf cnt((nout + 1) * 8);
+    cn_off.alloc((nout + 1) * 8);
     MB_CUDA(cudaMemsetAsync(cnt.p, 0, (nout + 1) * 8, stream));
     if (nout)
-      launch("tri_count", [&] {
-        k_triangles<0><<<grid_for(nout, 128), 128, 0, stream>>>(n, nout, out_off.as<uint64_t>(), out_nbr.as<uint32_t>(),
-                                                                out_slot.as<uint32_t>(), out_src.as<uint32_t>(),
-                                                                cnt.as<uint64_t>(), nullptr, nullptr);
+      launch("cn_count", [&] {
+        k_cn_build<0><<<grid_for(nout, 128), 128, 0, stream>>>(nout, out_off.as<uint64_t>(), out_nbr.as<uint32_t>(),
+                                                               out_slot.as<uint32_t>(), out_src.as<uint32_t>(),
+                                                               rev.as<uint32_t>(), reinterpret_cast<u64*>(cnt.p),
+                                                               nullptr, nullptr, nullptr, nullptr);
       });
-    exclusive_scan(cnt.as<uint64_t>(), toff.as<uint64_t>(), nout + 1);
-    MB_CUDA(cudaMemcpyAsync(&ntri, toff.as<uint64_t>() + nout, 8, cudaMemcpyDeviceToHost, stream));
+    exclusive_scan(cnt.as<uint64_t>(), cn_off.as<uint64_t>(), nout + 1);
+    uint64_t ncn_h = 0;
+    MB_CUDA(cudaMemcpyAsync(&ncn_h, cn_off.as<uint64_t>() + nout, 8, cudaMemcpyDeviceToHost, stream));
     MB_CUDA(cudaStreamSynchronize(stream));
-    tri.alloc(std::max<uint64_t>(ntri, 1) * 6 * sizeof(uint32_t));
-    if (nout && ntri)
-      launch("tri_fill", [&] {
-        k_triangles<1><<<grid_for(nout, 128), 128, 0, stream>>>(n, nout, out_off.as<uint64_t>(), out_nbr.as<uint32_t>(),
-                                                                out_slot.as<uint32_t>(), out_src.as<uint32_t>(),
-                                                                nullptr, toff.as<uint64_t>(), tri.as<uint32_t>());
+    ncn = ncn_h;
+    ntri = ncn / 3;
+    cn.alloc(std::max<uint64_t>(3 * ncn, 1) * sizeof(uint32_t));  // SoA: w | slot a->w | slot b->w
+    MB_CUDA(cudaMemsetAsync(cnt.p, 0, (nout + 1) * 8, stream));
+    if (nout && ncn)
+      launch("cn_fill", [&] {
+        k_cn_build<1><<<grid_for(nout, 128), 128, 0, stream>>>(nout, out_off.as<uint64_t>(), out_nbr.as<uint32_t>(),
+                                                               out_slot.as<uint32_t>(), out_src.as<uint32_t>(),
+                                                               rev.as<uint32_t>(), reinterpret_cast<u64*>(cnt.p),
+                                                               cn_off.as<uint64_t>(), cn.as<uint32_t>(), cn.as<uint32_t>() + ncn, cn.as<uint32_t>() + 2 * ncn);
       });
     MB_CUDA(cudaStreamSynchronize(stream));
+    this->nout = nout;
+    this->out_nbr = std::move(out_nbr);
+    this->out_slot = std::move(out_slot);
+    this->out_src = std::move(out_src);
     st.triangles = ntri;
     tri_ready = true;
+    st.prep_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   }
 
   void exclusive_scan(const uint64_t* in, uint64_t* out, uint64_t count) {
@@ -695,7 +559,15 @@ struct GpuEngine::Impl {
         for (int e = 0; e < sp.L; ++e)
           if (sp.edge_tab[e] >= 0 && tables[sp.edge_tab[e]].kind != TKind::Edge) edge_children_on_edges = false;
         static const bool force_general = std::getenv("MB_FORCE_GENERAL_CYCLES") != nullptr;
-        if (sp.L == 3 && edge_children_on_edges && out.kind != TKind::Pair && !force_general)
+        // the CN kernel keeps the pivot factors' partial products per edge in
+        // shared memory; bound them by the product of all factor widths
+        uint64_t fixed_bound = 1;
+        for (int q = 0; q < sp.L; ++q) {
+          if (sp.node_tab[q] >= 0) fixed_bound *= tables[sp.node_tab[q]].P;
+          if (sp.edge_tab[q] >= 0) fixed_bound *= tables[sp.edge_tab[q]].P;
+        }
+        if (sp.L == 3 && edge_children_on_edges && out.kind != TKind::Pair && !force_general &&
+            fixed_bound <= static_cast<uint64_t>(kTriFixedCap))
           needs_triangles = true;
         else
           sp.general = true;
@@ -756,6 +628,36 @@ struct GpuEngine::Impl {
     const size_t group_bytes = (A.PZ + A.Pout) * sizeof(u64);
     (void)per_group;
     if (group_bytes * 4 > 200 * 1024) fail(kSpec, "leaf table row too wide for shared memory (k too large)");
+    // compulsory bytes: CSR rows + neighbour colours + every input row once + output
+    const uint64_t leaf_bytes = 8 * (uint64_t(n) + 1) + 5 * m2 + n + (A.ub ? uint64_t(n) * A.Pb * 8 : 0) +
+                                (A.ua ? uint64_t(n) * A.Pa * 8 : 0) + (A.ue ? m2 * A.Pe * 8 : 0) +
+                                uint64_t(n) * out.P * 8;
+    // table-driven kernel (leaf.cuh) whenever the edge is a plain graph edge
+    LeafMapArgs M{};
+    M.off = A.off, M.adj = A.adj, M.chi = A.chi, M.ub = A.ub, M.ua = A.ua;
+    M.Pb = A.Pb, M.Pa = A.Pa, M.PZ = A.PZ, M.Pout = A.Pout, M.sb = A.sb, M.sa = A.sa, M.sZ = A.sZ, M.k = k;
+    M.out = A.out, M.err = err, M.updates = upd;
+    const size_t map_bytes = ((static_cast<size_t>(k) * k * (A.ub ? A.Pb : 1) * 2 + 7) / 8) * 8;
+    if (!A.ue && map_bytes + group_bytes * 8 <= 160 * 1024) {
+      if (nlight) {
+        const size_t smem = map_bytes + group_bytes * 8;  // 8 warps per CTA
+        if (smem > 48 * 1024)
+          MB_CUDA(cudaFuncSetAttribute(leaf_map_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((nlight + 7) / 8, 148 * 32));
+        launch("leaf_map", [&] { leaf_map_kernel<32><<<grid, 256, smem, stream>>>(M, vlight.as<uint32_t>(), nlight); },
+               leaf_bytes * (m2 ? double(slots_light) / m2 : 1.0));
+      }
+      if (nheavy) {
+        const size_t smem = map_bytes + group_bytes;
+        if (smem > 48 * 1024)
+          MB_CUDA(cudaFuncSetAttribute(leaf_map_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const unsigned grid = static_cast<unsigned>(std::min<uint64_t>(nheavy, 148 * 8));
+        launch("leaf_map_heavy",
+               [&] { leaf_map_kernel<256><<<grid, 256, smem, stream>>>(M, vheavy.as<uint32_t>(), nheavy); },
+               leaf_bytes * (m2 ? double(m2 - slots_light) / m2 : 0.0));
+      }
+      return;
+    }
     if (nlight) {
       const size_t smem = group_bytes * 4;  // 4 warps per CTA
       if (smem > 48 * 1024)
@@ -774,45 +676,71 @@ struct GpuEngine::Impl {
     }
   }
 
-  void run_triangle(const StepPlan& sp, int* err, u64* scalar, u64* upd) {
+  // 3-cycle block over the CN lists (tri_edge.cuh).  The pivot edge (P0, P1)
+  // is the boundary pair (|B| = 2), an edge at the boundary (|B| = 1) or an
+  // annotated edge when there is one, so the pivot-fixed factors are read once
+  // per graph edge.
+  void run_tri_edge(const StepPlan& sp, int* err, u64* scalar, u64* upd) {
     DevTable& out = tables[sp.block];
-    TriArgs A{};
-    A.tri = tri.as<uint32_t>();
-    A.ntri = ntri;
+    auto edge_idx = [](int a, int b) { return b == (a + 1) % 3 ? a : b; };
+    int P0 = 0, P1 = 1;
+    if (sp.bpos.size() == 2) {
+      P0 = sp.bpos[0], P1 = sp.bpos[1];
+    } else if (sp.bpos.size() == 1) {
+      P0 = sp.bpos[0];
+      const int nxt = (P0 + 1) % 3, prv = (P0 + 2) % 3;
+      P1 = (sp.edge_tab[edge_idx(P0, nxt)] < 0 && sp.edge_tab[edge_idx(P0, prv)] >= 0) ? prv : nxt;
+    } else {
+      for (int e = 0; e < 3; ++e)
+        if (sp.edge_tab[e] >= 0) {
+          P0 = e, P1 = (e + 1) % 3;
+          break;
+        }
+    }
+    const int P2 = 3 - P0 - P1;
+    TriEdgeArgs A{};
+    A.nout = nout;
+    A.cn_off = cn_off.as<uint64_t>();
+    A.cn_w = cn.as<uint32_t>(), A.cn_sa = A.cn_w + ncn, A.cn_sb = A.cn_w + 2 * ncn, A.k = k;
+    A.out_src = out_src.as<uint32_t>();
+    A.out_nbr = out_nbr.as<uint32_t>();
+    A.out_slot = out_slot.as<uint32_t>();
     A.rev = rev.as<uint32_t>();
     A.chi = chi.as<uint8_t>();
-    A.err = err;
-    A.updates = upd;
-    A.scalar = scalar;
-    int nf = 0;
-    for (int q = 0; q < 3; ++q) {
-      if (sp.node_tab[q] >= 0) {
-        const DevTable& t = tables[sp.node_tab[q]];
-        A.f[nf++] = Factor{t.data(), t.P, t.s, q, -1};
-      }
-    }
-    for (int e = 0; e < 3; ++e) {
-      if (sp.edge_tab[e] >= 0) {
-        const DevTable& t = tables[sp.edge_tab[e]];
-        const int a = e, b = (e + 1) % 3;
-        A.f[nf++] = sp.edge_fwd[e] ? Factor{t.data(), t.P, t.s, a, b} : Factor{t.data(), t.P, t.s, b, a};
-      }
-    }
-    A.nf = nf;
-    if (out.kind == TKind::Scalar) {
-      A.out_kind = 0;
-    } else if (out.kind == TKind::Vertex) {
-      A.out_kind = 1;
-      A.b0 = sp.bpos[0];
-    } else {
-      A.out_kind = 2;
-      A.b0 = sp.bpos[0];
-      A.b1 = sp.bpos[1];
-    }
+    A.err = err, A.updates = upd, A.scalar = scalar;
+    const bool per_w = sp.node_tab[P2] >= 0 || sp.edge_tab[edge_idx(P1, P2)] >= 0 || sp.edge_tab[edge_idx(P2, P0)] >= 0;
+    uint64_t bytes = (per_w ? 12 : 4) * ncn + 8 * (nout + 1) + 12 * nout + n + 4 * m2;
+    auto node = [&](int pos, const uint64_t*& t, uint32_t& P, int& s) {
+      if (sp.node_tab[pos] < 0) return;
+      const DevTable& d = tables[sp.node_tab[pos]];
+      t = d.data(), P = d.P, s = d.s;
+      bytes += d.buf.bytes;
+    };
+    auto edge = [&](int pa, int pb, const uint64_t*& t, uint32_t& P, int& s, int& sw) {
+      const int i = edge_idx(pa, pb);
+      if (sp.edge_tab[i] < 0) return;
+      const DevTable& d = tables[sp.edge_tab[i]];
+      const bool keyed_ab = (i == pa) ? sp.edge_fwd[i] : !sp.edge_fwd[i];
+      t = d.data(), P = d.P, s = d.s, sw = !keyed_ab;
+      bytes += d.buf.bytes;
+    };
+    node(P0, A.n0, A.Pn0, A.sn0);
+    node(P1, A.n1, A.Pn1, A.sn1);
+    node(P2, A.n2, A.Pn2, A.sn2);
+    edge(P0, P1, A.e01, A.Pe01, A.se01, A.sw01);
+    edge(P1, P2, A.e12, A.Pe12, A.se12, A.sw12);
+    edge(P2, P0, A.e20, A.Pe20, A.se20, A.sw20);
+    A.out_kind = out.kind == TKind::Scalar ? 0 : out.kind == TKind::Vertex ? 1 : 2;
     A.out = out.data();
     A.Pout = out.P;
-    if (ntri)
-      launch("triangle_block", [&] { triangle_block_kernel<<<grid_for(ntri * 6, 256), 256, 0, stream>>>(A); });
+    if (out.kind != TKind::Scalar) bytes += out.buf.bytes;
+    const size_t smem = static_cast<size_t>(kTriWarps) * (3 * kTriFixedCap + 2 * A.Pout + 2 + kMaxColors) * sizeof(u64);
+    if (smem > 48 * 1024)
+      MB_CUDA(cudaFuncSetAttribute(tri_edge_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((nout + kTriWarps - 1) / kTriWarps, 148 * 64));
+    if (nout)
+      launch("tri_edge_block", [&] { tri_edge_block_kernel<<<std::max(grid, 1u), 32 * kTriWarps, smem, stream>>>(A); },
+             bytes);
   }
 
   TabView view(int tab) const {
@@ -890,11 +818,13 @@ struct GpuEngine::Impl {
         });
       for (const StepPlan& sp : steps) {
         DevTable& out = tables[sp.block];
-        if (out.kind == TKind::Edge || (out.kind == TKind::Vertex && sp.kind == BlockKind::Cycle))
+        // outputs accumulated with atomics start from zero; the CN kernel writes
+        // every row of its edge outputs and the leaf kernels every vertex row
+        if ((out.kind == TKind::Edge && sp.general) || (out.kind == TKind::Vertex && sp.kind == BlockKind::Cycle))
           MB_CUDA(cudaMemsetAsync(out.buf.p, 0, out.buf.bytes, stream));
         if (sp.kind == BlockKind::Leaf) run_leaf(sp, err, upd);
         else if (sp.general) run_general(sp, err, scalar, upd);
-        else run_triangle(sp, err, scalar, upd);
+        else run_tri_edge(sp, err, scalar, upd);
       }
       if (plan.singleton_root) {
         const DevTable& t = tables[plan.root];
@@ -954,7 +884,11 @@ void GpuEngine::bind_plan(const Plan& plan, int k) { impl_->bind(plan, k); }
 void GpuEngine::count(const uint8_t* chi, int nc, bool host, uint64_t* out) { impl_->count(chi, nc, host, out); }
 void GpuEngine::reset_derived() {
   impl_->tri_ready = false;
-  impl_->tri.release();
+  impl_->cn.release();
+  impl_->cn_off.release();
+  impl_->out_nbr.release();
+  impl_->out_slot.release();
+  impl_->out_src.release();
 }
 void GpuEngine::enable_timing(bool on) {
   impl_->timing = on;

@@ -30,6 +30,7 @@ struct EngineStats {
   uint64_t table_bytes = 0;     // bytes of DP tables resident
   uint64_t dp_updates = 0;      // table-entry updates (nonzero contributions) of the last count
   double last_ms = 0;
+  double prep_ms = 0;           // wall time of the last plan-derived index build
 };
 
 class GpuEngine {

@@ -1,0 +1,114 @@
+// Leaf blocks, table-driven variant.  Included by engine.cu after its helpers.
+//
+// Path-table extension along CSR rows (paper §5.2 leaf blocks; reference
+// engine.cpp:368-382: edge table -> node join on the leaf -> node join on the
+// boundary -> projection to the boundary).  For a boundary vertex x the leaf
+// side contributes, for every neighbour y, the row U_b[y] shifted by x's
+// colour.  Which output colour-set index an entry (colour of x, colour of y,
+// entry ib of U_b's row) lands in depends only on (chi x, chi y, ib), so the
+// whole colour-set arithmetic is precomputed into a shared-memory map and the
+// inner loop is: load neighbour id, its colour, its row (vectorised), and add
+// into the shared accumulator through the map.
+//
+// Degree-binned scheduling: a warp per light vertex, a 256-thread CTA per
+// heavy vertex (degree > 256), so hubs do not serialise a warp.
+
+struct LeafMapArgs {
+  const uint64_t* off;
+  const uint32_t* adj;
+  const uint8_t* chi;
+  const uint64_t* ub;  // node child on the leaf (row = img b), may be null
+  const uint64_t* ua;  // node child on the boundary (row = img a), may be null
+  uint32_t Pb, Pa, PZ, Pout;
+  int sb, sa, sZ, k;
+  uint64_t* out;
+  int* err;
+  u64* updates;
+};
+
+// map entry for (cx, cy, ib): Z index, or 0xFFFF when chi x is in the leaf's set
+__device__ __forceinline__ uint32_t leaf_map_size(const LeafMapArgs& A) {
+  return static_cast<uint32_t>(A.k) * A.k * (A.ub ? A.Pb : 1u);
+}
+
+template <int GROUP>
+__global__ void __launch_bounds__(256)
+leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) {
+  extern __shared__ u64 lsm[];
+  const int kThreads = blockDim.x;
+  const int kGroups = kThreads / GROUP;
+  const uint32_t msize = leaf_map_size(A);
+  uint16_t* map = reinterpret_cast<uint16_t*>(lsm);
+  u64* acc = lsm + (msize * 2 + 7) / 8;
+  const uint32_t pb = A.ub ? A.Pb : 1u;
+  for (uint32_t i = threadIdx.x; i < msize; i += kThreads) {
+    const uint32_t ib = i % pb, cy = (i / pb) % A.k, cx = i / (pb * A.k);
+    uint16_t t = 0xFFFF;
+    if (cx != cy) {
+      const uint32_t fx = 1u << cx, fy = 1u << cy;
+      const uint32_t Mb = A.ub ? sig_expand(sig_unrank(c_lut, A.sb - 1, ib), fy) : fy;
+      if (!(Mb & fx)) t = static_cast<uint16_t>(sig_index(c_lut, Mb | fx, fx));
+    }
+    map[i] = t;
+  }
+  __syncthreads();
+  const int g = threadIdx.x / GROUP, lane = threadIdx.x % GROUP;
+  u64* Z = acc + static_cast<size_t>(g) * (A.PZ + A.Pout);
+  u64* O = Z + A.PZ;
+  uint64_t upd = 0;
+  for (uint32_t gi = blockIdx.x * kGroups + g; gi < nv; gi += gridDim.x * kGroups) {
+    const uint32_t x = vlist[gi];
+    for (uint32_t i = lane; i < A.PZ + A.Pout; i += GROUP) Z[i] = 0;
+    if (GROUP == 32) __syncwarp(); else __syncthreads();
+    const uint32_t cx = A.chi[x];
+    const uint64_t base = A.off[x], deg = A.off[x + 1] - base;
+    const uint16_t* mx = map + static_cast<size_t>(cx) * A.k * pb;
+    for (uint64_t j = lane; j < deg; j += GROUP) {
+      const uint32_t y = __ldg(A.adj + base + j);
+      const uint32_t cy = __ldg(A.chi + y);
+      const uint16_t* my = mx + cy * pb;
+      if (!A.ub) {
+        const uint16_t t = my[0];
+        if (t != 0xFFFF) {
+          atomicAdd(Z + t, 1ull);
+          ++upd;
+        }
+        continue;
+      }
+      if (cy == cx) continue;
+      const uint64_t* row = A.ub + static_cast<uint64_t>(y) * pb;
+      for (uint32_t ib = 0; ib < pb; ++ib) {
+        const uint64_t v = __ldg(row + ib);
+        if (!v) continue;
+        const uint16_t t = my[ib];
+        if (t == 0xFFFF) continue;
+        atomic_add_ck(Z + t, v, A.err);
+        ++upd;
+      }
+    }
+    if (GROUP == 32) __syncwarp(); else __syncthreads();
+    if (!A.ua) {
+      for (uint32_t i = lane; i < A.Pout; i += GROUP) A.out[static_cast<uint64_t>(x) * A.Pout + i] = Z[i];
+    } else {
+      const uint32_t fx = 1u << cx;
+      const uint64_t items = static_cast<uint64_t>(A.PZ) * A.Pa;
+      for (uint64_t it = lane; it < items; it += GROUP) {
+        const uint32_t iz = static_cast<uint32_t>(it / A.Pa), ia = static_cast<uint32_t>(it - iz * A.Pa);
+        const uint64_t z = Z[iz];
+        if (!z) continue;
+        const uint64_t a = __ldg(A.ua + static_cast<uint64_t>(x) * A.Pa + ia);
+        if (!a) continue;
+        const uint32_t Mz = sig_expand(sig_unrank(c_lut, A.sZ - 1, iz), fx);
+        const uint32_t Ma = sig_expand(sig_unrank(c_lut, A.sa - 1, ia), fx);
+        if ((Mz & Ma) != fx) continue;
+        atomic_add_ck(O + sig_index(c_lut, Mz | Ma, fx), mul_ck(z, a, A.err), A.err);
+        ++upd;
+      }
+      if (GROUP == 32) __syncwarp(); else __syncthreads();
+      for (uint32_t i = lane; i < A.Pout; i += GROUP) A.out[static_cast<uint64_t>(x) * A.Pout + i] = O[i];
+    }
+    if (GROUP == 32) __syncwarp(); else __syncthreads();
+  }
+  for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(0xffffffffu, upd, o);
+  if ((threadIdx.x & 31) == 0 && upd) atomicAdd(A.updates, static_cast<u64>(upd));
+}
