@@ -734,6 +734,36 @@ struct GpuEngine::Impl {
     A.out = out.data();
     A.Pout = out.P;
     if (out.kind != TKind::Scalar) bytes += out.buf.bytes;
+    // histogram path (tri_hist_kernel): nothing depends on the third vertex
+    // and at most one factor sits on the pivot
+    const int nfixed = (A.n0 != nullptr) + (A.n1 != nullptr) + (A.e01 != nullptr);
+    if (!per_w && nfixed <= 1) {
+      TriHistArgs H{};
+      H.nout = nout;
+      H.cn_off = A.cn_off, H.cn_w = A.cn_w, H.out_src = A.out_src, H.out_nbr = A.out_nbr;
+      H.out_slot = A.out_slot, H.rev = A.rev, H.chi = A.chi, H.k = k;
+      H.s_out = sp.s_out;
+      H.P2 = static_cast<uint32_t>(binom(k - 2, sp.s_out - 2));
+      H.nterm = sp.s_out - 2;
+      if (A.n0) H.fkind = 1, H.F = A.n0, H.PF = A.Pn0;
+      else if (A.n1) H.fkind = 2, H.F = A.n1, H.PF = A.Pn1;
+      else if (A.e01) H.fkind = 3, H.F = A.e01, H.PF = A.Pe01, H.sw01 = A.sw01;
+      H.out_kind = A.out_kind, H.out = A.out, H.Pout = A.Pout;
+      H.scalar = scalar, H.err = err, H.updates = upd;
+      const size_t tsize = static_cast<size_t>(k) * k * H.P2 * H.nterm;
+      const size_t isize = H.out_kind == 1 ? static_cast<size_t>(k) * k * H.P2 : 0;
+      const size_t hsmem = (tsize + (isize + 1) / 2 + static_cast<size_t>(kHistWarps) * 32 * k) * 4;
+      if (hsmem <= 200 * 1024) {
+        if (hsmem > 48 * 1024)
+          MB_CUDA(cudaFuncSetAttribute(tri_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hsmem));
+        const uint64_t nbatch = (nout + 31) / 32;
+        const unsigned grid = static_cast<unsigned>(
+            std::max<uint64_t>(1, std::min<uint64_t>((nbatch + kHistWarps - 1) / kHistWarps, 148 * 8)));
+        if (nout)
+          launch("tri_hist", [&] { tri_hist_kernel<<<grid, 32 * kHistWarps, hsmem, stream>>>(H); }, bytes);
+        return;
+      }
+    }
     const size_t smem = static_cast<size_t>(kTriWarps) * (3 * kTriFixedCap + 2 * A.Pout + 2 + kMaxColors) * sizeof(u64);
     if (smem > 48 * 1024)
       MB_CUDA(cudaFuncSetAttribute(tri_edge_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -353,3 +353,160 @@ __global__ void __launch_bounds__(32 * kTriWarps) tri_edge_block_kernel(TriEdgeA
   for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(0xffffffffu, upd, o);
   if (lane == 0 && upd) atomicAdd(A.updates, static_cast<u64>(upd));
 }
+
+// ---------------------------------------------------------------------------
+// Histogram path, batched: one warp owns 32 consecutive oriented edges.
+//
+// (1) The warp scans the 32 edges' CN lists as one flat, coalesced range
+//     (lane i reads entries i, i+32, ...), finds each entry's edge by a
+//     5-step search over the 33 offsets and bumps hist[edge][chi(w)] in
+//     shared memory.
+// (2) Lane l then evaluates edge j0+l.  An output entry S (a colour set that
+//     contains the pivot colours c0, c1) receives
+//         sum over c in S \ {c0, c1} of hist[c] * F[S \ {c}]
+//     where F is the single pivot factor (node row at P0 or P1, edge row of
+//     the pivot, or the bare edge).  Which (c, F-index) pairs feed entry S
+//     depends only on (c0, c1, S), so the CTA precomputes them once into a
+//     shared table `terms[c0][c1][i][t]` and the lane does loads and
+//     multiply-adds only.
+// ---------------------------------------------------------------------------
+
+struct TriHistArgs {
+  uint64_t nout;
+  const uint64_t* cn_off;
+  const uint32_t* cn_w;
+  const uint32_t* out_src;
+  const uint32_t* out_nbr;
+  const uint32_t* out_slot;
+  const uint32_t* rev;
+  const uint8_t* chi;
+  int k;
+  int s_out;      // popcount of the block's signatures
+  uint32_t P2;    // C(k-2, s_out-2): entries of S containing both pivot colours
+  int nterm;      // s_out - 2
+  int fkind;      // pivot factor: 0 none, 1 node at P0, 2 node at P1, 3 edge (P0,P1)
+  const uint64_t* F;
+  uint32_t PF;
+  int sw01;       // edge factor stored keyed (P1, P0)
+  int out_kind;   // 0 scalar, 1 unary keyed by img P0, 2 edge keyed (img P0, img P1)
+  uint64_t* out;
+  uint32_t Pout;
+  u64* scalar;
+  int* err;
+  u64* updates;
+};
+
+constexpr int kHistWarps = 8;
+
+__global__ void __launch_bounds__(32 * kHistWarps) tri_hist_kernel(TriHistArgs A) {
+  extern __shared__ uint32_t hsm[];
+  const int k = A.k;
+  const uint32_t tsize = static_cast<uint32_t>(k) * k * A.P2 * A.nterm;
+  uint32_t* terms = hsm;                                   // [k][k][P2][nterm]  (c << 16) | j, or ~0
+  uint16_t* idx1 = reinterpret_cast<uint16_t*>(hsm + tsize);  // [k][k][P2] unary output index
+  const uint32_t isize = A.out_kind == 1 ? static_cast<uint32_t>(k) * k * A.P2 : 0;
+  uint32_t* hist_all = hsm + tsize + (isize + 1) / 2;      // [warps][32][k]
+  // ---- per-CTA term table
+  for (uint32_t e = threadIdx.x; e < static_cast<uint32_t>(k) * k * A.P2; e += blockDim.x) {
+    const uint32_t i = e % A.P2, c1 = (e / A.P2) % k, c0 = e / (A.P2 * k);
+    if (c0 == c1) continue;
+    const uint32_t f2 = (1u << c0) | (1u << c1);
+    const uint32_t S = sig_expand(sig_unrank(c_lut, A.s_out - 2, i), f2);
+    if (A.out_kind == 1) idx1[e] = static_cast<uint16_t>(sig_index(c_lut, S, 1u << c0));
+    uint32_t free = S & ~f2;
+    for (int t = 0; t < A.nterm; ++t) {
+      const int c = mb_ctz(free);
+      free &= free - 1u;
+      const uint32_t T = S & ~(1u << c);
+      uint32_t j = 0;
+      bool ok = true;
+      switch (A.fkind) {
+        case 0: ok = T == f2; break;
+        case 1: j = sig_index(c_lut, T & ~(1u << c1), 1u << c0); break;
+        case 2: j = sig_index(c_lut, T & ~(1u << c0), 1u << c1); break;
+        default: j = sig_index(c_lut, T, f2); break;
+      }
+      terms[static_cast<size_t>(e) * A.nterm + t] = ok ? (static_cast<uint32_t>(c) << 16) | j : ~0u;
+    }
+  }
+  __syncthreads();
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint32_t* hist = hist_all + static_cast<size_t>(wid) * 32 * k;
+  uint64_t local = 0, upd = 0;
+  const uint64_t nbatch = (A.nout + 31) / 32;
+  for (uint64_t bt = static_cast<uint64_t>(blockIdx.x) * kHistWarps + wid; bt < nbatch;
+       bt += static_cast<uint64_t>(gridDim.x) * kHistWarps) {
+    const uint64_t j0 = bt * 32;
+    const uint64_t j = j0 + lane;
+    const bool live = j < A.nout;
+    for (int i = lane; i < 32 * k; i += 32) hist[i] = 0;
+    // lane l holds offset of edge j0+l (and lane 31's end via shuffle)
+    const uint64_t myoff = A.cn_off[live ? j : A.nout];
+    const uint64_t endoff = A.cn_off[min(j0 + 32, A.nout)];
+    const uint64_t startoff = __shfl_sync(0xffffffffu, myoff, 0);
+    __syncwarp();
+    for (uint64_t e0 = startoff; e0 < endoff; e0 += 32) {
+      const uint64_t e = e0 + lane;
+      // edge of entry e: last lane l with off(l) <= e (binary search over the
+      // lanes' offsets; all lanes take part in every shuffle)
+      int lo = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1) {
+        const uint64_t o = __shfl_sync(0xffffffffu, myoff, lo + step);
+        if (o <= e) lo += step;
+      }
+      if (e < endoff) atomicAdd(hist + lo * k + A.chi[__ldg(A.cn_w + e)], 1u);
+    }
+    __syncwarp();
+    if (live) {
+      const uint32_t a = A.out_src[j], b = A.out_nbr[j];
+      const uint32_t sab = A.out_slot[j], sba = A.rev[sab];
+      const uint32_t ca = A.chi[a], cb = A.chi[b];
+      const uint32_t* h = hist + lane * k;
+      for (int o = 0; o < 2; ++o) {
+        const uint32_t c0 = o ? cb : ca, c1 = o ? ca : cb;
+        const uint64_t orow = static_cast<uint64_t>(o ? sba : sab) * A.Pout;
+        if (c0 == c1) {
+          if (A.out_kind == 2)
+            for (uint32_t i = 0; i < A.Pout; ++i) A.out[orow + i] = 0;
+          continue;
+        }
+        const uint64_t* F = nullptr;
+        if (A.fkind == 1) F = A.F + static_cast<uint64_t>(o ? b : a) * A.PF;
+        else if (A.fkind == 2) F = A.F + static_cast<uint64_t>(o ? a : b) * A.PF;
+        else if (A.fkind == 3) F = A.F + static_cast<uint64_t>((o == 0) != (A.sw01 != 0) ? sab : sba) * A.PF;
+        const uint32_t tb = (c0 * k + c1) * A.P2;
+        for (uint32_t i = 0; i < A.P2; ++i) {
+          const uint32_t* tt = terms + static_cast<size_t>(tb + i) * A.nterm;
+          uint64_t v = 0;
+          for (int t = 0; t < A.nterm; ++t) {
+            const uint32_t x = tt[t];
+            if (x == ~0u) continue;
+            const uint32_t hc = h[x >> 16];
+            if (!hc) continue;
+            const uint64_t f = F ? __ldg(F + (x & 0xFFFFu)) : 1ull;
+            if (!f) continue;
+            v = add_ck(v, mul_ck(f, hc, A.err), A.err);
+            ++upd;
+          }
+          if (A.out_kind == 2) {
+            A.out[orow + i] = v;
+          } else if (v) {
+            if (A.out_kind == 0)
+              local = add_ck(local, v, A.err);
+            else
+              atomic_add_ck(reinterpret_cast<u64*>(A.out) + static_cast<uint64_t>(o ? b : a) * A.Pout +
+                                idx1[tb + i], v, A.err);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+  if (A.out_kind == 0) {
+    for (int o = 16; o > 0; o >>= 1) local = add_ck(local, __shfl_down_sync(0xffffffffu, local, o), A.err);
+    if (lane == 0 && local) atomic_add_ck(A.scalar, local, A.err);
+  }
+  for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(0xffffffffu, upd, o);
+  if (lane == 0 && upd) atomicAdd(A.updates, static_cast<u64>(upd));
+}
