@@ -1,0 +1,96 @@
+"""Multi-GPU counting: one process per GPU, colourings sharded across ranks.
+
+The reference parallelises one colouring's DP over p workers with a 1-D
+vertex partition and entry exchange between rounds (runtime.hpp:14-88,
+BspExecutor), and estimate() runs trials in parallel threads
+(estimate.cpp:149).  On B200 a whole colouring of the benchmark graphs fits
+one GPU (the largest config's tables are a few GB of 180 GB HBM), so the
+independent units are the colourings: rank r counts the contiguous block of
+colourings that Partition(num_colourings, world).block(r) assigns it, with no
+data-path collective, and the per-colouring counts are all-gathered once at
+the end (NCCL on GPUs, gloo on CPU).  Results are bit-identical to the
+single-GPU call for every world size.
+
+``count_fn`` lets the CPU tests drive the same plumbing with the oracle.
+"""
+from __future__ import annotations
+
+from typing import Callable, Sequence
+
+import numpy as np
+
+from . import EstimateReport, automorphism_count, coefficient_of_variation, derive_seed, normalization_factor
+
+
+def block(n: int, world: int, rank: int) -> tuple[int, int]:
+    """[begin, end) of rank's block: Partition(n, p) (runtime.hpp:14-25);
+    the first n % p ranks hold one extra item; empty blocks when n < p."""
+    base, rem = divmod(n, world)
+    begin = rank * base + min(rank, rem)
+    return begin, begin + base + (1 if rank < rem else 0)
+
+
+def _world():
+    import torch.distributed as dist
+
+    if dist.is_available() and dist.is_initialized():
+        return dist, dist.get_world_size(), dist.get_rank()
+    return None, 1, 0
+
+
+def _all_gather_counts(local: np.ndarray, total: int, dist, world: int, device) -> np.ndarray:
+    import torch
+
+    # pad every rank's block to the largest block, gather, then trim
+    width = -(-total // world)
+    buf = torch.zeros(width, dtype=torch.int64, device=device)
+    if len(local):
+        buf[: len(local)] = torch.from_numpy(local.astype(np.uint64).view(np.int64)).to(device)
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf)
+    out = []
+    for r in range(world):
+        b, e = block(total, world, r)
+        out.append(parts[r][: e - b].cpu().numpy().view(np.uint64))
+    return np.concatenate(out) if out else np.zeros(0, np.uint64)
+
+
+def distributed_count_seeds(g, plan, seeds: Sequence[int], engine: int = 1,
+                            count_fn: Callable | None = None, device=None) -> np.ndarray:
+    """Colourful counts for the colourings random_coloring(n, k, seed) of every
+    seed, computed across all ranks; every rank returns the full list."""
+    from . import count_colorful_seeds
+
+    dist, world, rank = _world()
+    b, e = block(len(seeds), world, rank)
+    mine = list(seeds[b:e])
+    if count_fn is not None:
+        local = np.asarray([count_fn(s) for s in mine], dtype=np.uint64)
+    else:
+        local = count_colorful_seeds(g, plan, mine, engine) if mine else np.zeros(0, np.uint64)
+    if world == 1:
+        return local
+    if device is None:
+        import torch
+
+        device = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else "cpu"
+    return _all_gather_counts(local, len(seeds), dist, world, device)
+
+
+def distributed_estimate(g, plan, engine: int, trials: int, seed: int, k: int | None = None,
+                         edges=None, count_fn: Callable | None = None, device=None) -> EstimateReport:
+    """estimate() (estimate.hpp:34) with the trials sharded over the ranks.
+    Trial i uses derive_seed(seed, i) exactly as the single-process call, so
+    the report is identical for every world size."""
+    if trials < 1:
+        raise ValueError("trials must be >= 1")
+    k = plan.k if k is None else k
+    edges = plan.edges if edges is None else edges
+    seeds = [derive_seed(seed, i) for i in range(trials)]
+    per = distributed_count_seeds(g, plan, seeds, engine, count_fn, device)
+    norm = normalization_factor(k)
+    total = sum(int(x) for x in per)
+    mean = norm * (total / trials)
+    aut = automorphism_count(k, edges)
+    return EstimateReport(trials, [int(x) for x in per], norm, mean, coefficient_of_variation(per), aut,
+                          mean / aut)

@@ -1,0 +1,86 @@
+"""Multi-rank plumbing (paper_1602_04478_b200.parallel) on CPU: world size 2
+over gloo, with the oracle's brute-force count standing in for the device
+call.  The gathered per-trial counts and the estimate report must equal the
+reference's single-process estimate (tests/golden/estimates.json)."""
+import json
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, results):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_1602_04478_b200 as mb
+        from paper_1602_04478_b200 import parallel
+        from oracle import Oracle
+
+        O = Oracle()
+        gold = json.load(open(os.path.join(ROOT, "tests", "golden", "counts.json")))
+        plans = json.load(open(os.path.join(ROOT, "tests", "golden", "plans.json")))
+        est = json.load(open(os.path.join(ROOT, "tests", "golden", "estimates.json")))
+        out = []
+        for e in est:
+            g = gold["graphs"][e["graph"]]
+            p = plans[e["query"]]
+            off, adj, _ = O.build_csr(g["n"], g["edges"])
+            fn = lambda s, g=g, p=p, off=off, adj=adj: O.brute(off, adj, p["k"], p["edges"],
+                                                               O.random_coloring(g["n"], p["k"], s))
+            plan = mb.QueryPlan(p["k"], p["edges"])
+            rep = parallel.distributed_estimate(None, plan, 1, e["trials"], e["seed"], count_fn=fn, device="cpu")
+            out.append((rep.per_trial_colorful, rep.mean_estimate, rep.cv, rep.subgraph_estimate))
+        # uneven shards: 3 seeds over 2 ranks, 1 seed over 2 ranks
+        g = gold["graphs"]["er24"]
+        off, adj, _ = O.build_csr(g["n"], g["edges"])
+        c3 = [(0, 1), (1, 2), (2, 0)]
+        fn = lambda s: O.brute(off, adj, 3, c3, O.random_coloring(g["n"], 3, s))
+        three = parallel.distributed_count_seeds(None, None, [5, 6, 7], count_fn=fn, device="cpu")
+        one = parallel.distributed_count_seeds(None, None, [9], count_fn=fn, device="cpu")
+        results[rank] = (out, three.tolist(), one.tolist(), [fn(5), fn(6), fn(7)], [fn(9)])
+    finally:
+        dist.destroy_process_group()
+
+
+def test_block_partition():
+    from paper_1602_04478_b200.parallel import block
+
+    for n in (0, 1, 7, 64, 1001):
+        for w in (1, 2, 3, 8):
+            spans = [block(n, w, r) for r in range(w)]
+            assert spans[0][0] == 0 and spans[-1][1] == n
+            assert all(spans[i][1] == spans[i + 1][0] for i in range(w - 1))
+            sizes = [e - b for b, e in spans]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def test_two_ranks_gloo_estimate_matches_reference():
+    est = json.load(open(os.path.join(ROOT, "tests", "golden", "estimates.json")))
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_worker, args=(2, _free_port(), results), nprocs=2, join=True)
+    for rank in (0, 1):
+        out, three, one, three_want, one_want = results[rank]
+        assert three == three_want and one == one_want
+        for (per, mean, cv, sub), e in zip(out, est):
+            assert per == e["per_trial"]
+            assert mean == pytest.approx(e["mean"], rel=1e-12)
+            assert cv == pytest.approx(e["cv"], rel=1e-12, abs=1e-300)
+            assert sub == pytest.approx(e["subgraph"], rel=1e-12)
