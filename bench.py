@@ -295,7 +295,7 @@ def our_arm(args, cfg, ws, rank, local):
     step()
     timings = mb.engine_timings(g)
     mb.engine_enable_timing(g, False)
-    dp = [t for t in timings if t[0].startswith(("leaf_", "triangle", "tri_edge", "cycle_"))]
+    dp = [t for t in timings if t[0].startswith(("leaf_", "tri_", "cycle_"))]
     total_dp_ms = sum(t[1] for t in dp)
     top = max(dp, key=lambda t: t[1])
     peaks = measured_peaks()
