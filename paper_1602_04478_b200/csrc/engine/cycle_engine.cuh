@@ -24,7 +24,10 @@ struct TabView {
   int kind = 0;  // 0 none, 1 scalar, 2 vertex, 3 edge, 4 pair
   int s = 0;
   uint32_t P = 0;
-  uint64_t* data = nullptr;
+  uint32_t rs = 0;  // row stride (vertex/edge tables are [row][colouring][P]); pair tables: P
+  uint64_t* data = nullptr;  // pre-offset to the colouring's slice
+  uint64_t size = 0;         // readable elements from data (bounds checks)
+  uint64_t size_t_ = 0;      // readable elements from data_t
   // pair tables: CSR by first key (off[n+1], cols) and its transpose
   const uint64_t* off = nullptr;
   const uint32_t* cols = nullptr;
@@ -40,8 +43,12 @@ struct GraphView {
   const uint32_t* adj;
   const uint32_t* rev;
   const uint32_t* rank;
-  const uint8_t* chi;
+  const uint8_t* chi;  // pre-offset to the colouring; stride kChiStride
 };
+
+__device__ __forceinline__ uint32_t vcol(const GraphView& G, uint32_t v) {
+  return G.chi[static_cast<uint64_t>(v) * kChiStride];
+}
 
 struct HopArgs {
   GraphView G;
@@ -67,6 +74,8 @@ struct HopArgs {
   uint32_t Pn;
   int sn;
   int record;            // the new position is the recorded boundary
+  uint32_t rse, rsn;     // row strides of etab / ntab
+  uint64_t n_etab, n_ntab;  // readable elements from etab / ntab (bounds checks)
   // output contributions
   int s_out;
   uint32_t P_out;
@@ -118,20 +127,35 @@ __global__ void __launch_bounds__(256) k_hop_expand(HopArgs A) {
   const uint64_t i = lo;
   uint32_t x, v, r;
   unpack_key(A.key_in[i], A.in_has_r, A.bits, x, v, r);
+  if (x >= A.G.n || v >= A.G.n) {
+    atomicOr(A.err, 32);
+    A.key_out[item] = ~0ull;
+    return;
+  }
   const uint64_t slot = A.roff[v] + (item - A.woff[i]);
+  if (slot >= A.roff[A.G.n]) {
+    atomicOr(A.err, 64);
+    A.key_out[item] = ~0ull;
+    return;
+  }
   const uint32_t w = A.radj[slot];
+  if (w >= A.G.n) {
+    atomicOr(A.err, 128);
+    A.key_out[item] = ~0ull;
+    return;
+  }
   uint64_t* row = A.row_out + item * A.P_out;
   for (uint32_t j = 0; j < A.P_out; ++j) row[j] = 0;
   uint64_t key = ~0ull;
   bool any = false;
   if (A.G.rank[w] < A.G.rank[x]) {
-    const uint32_t cx = A.G.chi[x], cv = A.G.chi[v], cw = A.G.chi[w];
+    const uint32_t cx = vcol(A.G, x), cv = vcol(A.G, v), cw = vcol(A.G, w);
     const uint32_t fin = A.first_hop ? (1u << cx) : ((1u << cx) | (1u << cv));
     const uint32_t fout = (1u << cx) | (1u << cw);
     const uint32_t fw = 1u << cw, fv = 1u << cv;
     const uint64_t* prow = A.pay_in + i * A.P_in;
     const int t_in = A.s_in - mb_popc(fin);
-    const uint64_t erow = A.etab ? (A.e_rev ? A.G.rev[slot] : slot) * A.Pe : 0;
+    const uint64_t erow = A.etab ? (A.e_rev ? A.G.rev[slot] : slot) * A.rse : 0;
     for (uint32_t ii = 0; ii < A.P_in; ++ii) {
       const uint64_t pv = prow[ii];
       if (!pv) continue;
@@ -142,6 +166,10 @@ __global__ void __launch_bounds__(256) k_hop_expand(HopArgs A) {
         uint32_t S1;
         uint64_t v1;
         if (A.etab) {
+          if (erow + ie >= A.n_etab) {
+            atomicOr(A.err, 256);
+            continue;
+          }
           const uint64_t ev = A.etab[erow + ie];
           if (!ev) continue;
           const uint32_t E = sig_expand(sig_unrank(c_lut, A.se - 2, ie), fv | fw);
@@ -157,7 +185,11 @@ __global__ void __launch_bounds__(256) k_hop_expand(HopArgs A) {
           uint32_t S2;
           uint64_t v2;
           if (A.ntab) {
-            const uint64_t nv = A.ntab[static_cast<uint64_t>(w) * A.Pn + in];
+            if (static_cast<uint64_t>(w) * A.rsn + in >= A.n_ntab) {
+              atomicOr(A.err, 512);
+              continue;
+            }
+            const uint64_t nv = A.ntab[static_cast<uint64_t>(w) * A.rsn + in];
             if (!nv) continue;
             const uint32_t Nn = sig_expand(sig_unrank(c_lut, A.sn - 1, in), fw);
             if ((Nn & S1) != fw) continue;
@@ -168,6 +200,10 @@ __global__ void __launch_bounds__(256) k_hop_expand(HopArgs A) {
             v2 = v1;
           }
           const uint32_t o = sig_index(c_lut, S2, fout);
+          if (o >= A.P_out || mb_popc(S2) != A.s_out) {
+            atomicOr(A.err, 16);  // signature outside the frontier row: plan/popcount bug
+            continue;
+          }
           row[o] = add_ck(row[o], v2, A.err);
           any = true;
         }
@@ -208,14 +244,14 @@ __global__ void k_seg_accumulate(const uint64_t* __restrict__ keys, const uint64
 }
 
 __global__ void k_init_frontier(uint32_t x0, uint32_t nx, int bits, const uint8_t* __restrict__ chi,
-                                const uint64_t* __restrict__ utab, uint32_t Pu, uint64_t* __restrict__ key,
-                                uint64_t* __restrict__ pay) {
+                                const uint64_t* __restrict__ utab, uint32_t Pu, uint32_t rsu,
+                                uint64_t* __restrict__ key, uint64_t* __restrict__ pay) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nx) return;
   const uint64_t x = x0 + i;
   key[i] = (x << bits) | x;
   if (utab) {
-    for (uint32_t j = 0; j < Pu; ++j) pay[static_cast<uint64_t>(i) * Pu + j] = utab[x * Pu + j];
+    for (uint32_t j = 0; j < Pu; ++j) pay[static_cast<uint64_t>(i) * Pu + j] = utab[x * rsu + j];
   } else {
     pay[i] = 1;  // signature {chi x}
   }
@@ -242,7 +278,7 @@ struct MergeArgs {
   uint64_t* crow;   // pair: [nA][Pout]
   int key_src0, key_src1;  // 0 = x, 1 = v, 2 = r
   uint64_t* out;
-  uint32_t Pout;
+  uint32_t Pout, rso;
   u64* scalar;
   int* err;
   u64* updates;
@@ -273,30 +309,32 @@ __global__ void __launch_bounds__(256) k_half_merge(MergeArgs A) {
       A.ckey[i] = ~0ull;
       for (uint32_t j = 0; j < A.Pout; ++j) A.crow[i * A.Pout + j] = 0;
     }
-    if (lo < A.nB && A.keyB[lo] == kb) {
-      const uint32_t cx = A.G.chi[x], cv = A.G.chi[v];
+    bool found = lo < A.nB && A.keyB[lo] == kb;
+    uint64_t orow = 0;
+    uint32_t ofix = 0;
+    const uint32_t ids[3] = {x, v, r};
+    if (found && A.out_kind == 3) {
+      const uint32_t p = ids[A.key_src0], q = ids[A.key_src1];
+      const uint64_t s = find_slot(A.G, p, q);
+      if (s == ~0ull) {
+        atomicOr(A.err, 4);  // pair not adjacent: plan/table kind mismatch
+        found = false;
+      }
+      orow = s * A.rso;
+      ofix = (1u << vcol(A.G, p)) | (1u << vcol(A.G, q));
+    }
+    if (found) {
+      const uint32_t cx = vcol(A.G, x), cv = vcol(A.G, v);
       const uint32_t fx = 1u << cx, fv = 1u << cv, f2 = fx | fv;
-      const uint32_t ids[3] = {x, v, r};
-      uint64_t orow = 0;
-      uint32_t ofix = 0;
       if (A.out_kind == 2) {
         const uint32_t y = ids[A.key_src0];
-        orow = static_cast<uint64_t>(y) * A.Pout;
-        ofix = 1u << A.G.chi[y];
-      } else if (A.out_kind == 3) {
-        const uint32_t p = ids[A.key_src0], q = ids[A.key_src1];
-        const uint64_t s = find_slot(A.G, p, q);
-        if (s == ~0ull) {
-          atomicOr(A.err, 4);  // pair not adjacent: plan/table kind mismatch
-          return;
-        }
-        orow = s * A.Pout;
-        ofix = (1u << A.G.chi[p]) | (1u << A.G.chi[q]);
+        orow = static_cast<uint64_t>(y) * A.rso;
+        ofix = 1u << vcol(A.G, y);
       } else if (A.out_kind == 4) {
         const uint32_t p = ids[A.key_src0], q = ids[A.key_src1];
         A.ckey[i] = (static_cast<uint64_t>(p) << A.bits) | q;
         orow = i * A.Pout;
-        ofix = (1u << A.G.chi[p]) | (1u << A.G.chi[q]);
+        ofix = (1u << vcol(A.G, p)) | (1u << vcol(A.G, q));
       }
       const uint64_t* ra = A.payA + i * A.PA;
       const uint64_t* rb = A.payB + lo * A.PB;
@@ -356,7 +394,8 @@ struct Relation {
   const uint64_t* off;
   const uint32_t* adj;
   const uint64_t* pay = nullptr;  // per-slot payload rows (null: plain graph edges)
-  uint32_t P = 0;
+  uint64_t size = 0;              // readable elements from pay
+  uint32_t P = 0, rs = 0;         // entries per row, row stride
   int s = 0;
   int use_rev = 0;                // payload row = rev[slot] (edge tables walked backwards)
 };
@@ -424,8 +463,10 @@ struct CycleRunner {
     size_t tmp = 0;
     MB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, static_cast<int64_t>(W), 0, 64, stream));
     if (sort_tmp.bytes < tmp) sort_tmp.alloc(tmp);
-    MB_CUDA(cub::DeviceRadixSort::SortPairs(sort_tmp.p, tmp, kin, kout, vin, vout, static_cast<int64_t>(W), 0, 64,
-                                            stream));
+    launch("cub_radix_sort", [&] {
+      MB_CUDA(cub::DeviceRadixSort::SortPairs(sort_tmp.p, tmp, kin, kout, vin, vout, static_cast<int64_t>(W), 0, 64,
+                                              stream));
+    });
   }
 
   // Sort contributions (keys[W], rows[W][P]) and add equal keys: the
@@ -486,8 +527,8 @@ struct CycleRunner {
     A.W = W;
     A.roff = rel.off;
     A.radj = rel.adj;
-    if (rel.pay) A.etab = rel.pay, A.Pe = rel.P, A.se = rel.s, A.e_rev = rel.use_rev;
-    if (nt.kind) A.ntab = nt.data, A.Pn = nt.P, A.sn = nt.s;
+    if (rel.pay) A.etab = rel.pay, A.Pe = rel.P, A.rse = rel.rs, A.se = rel.s, A.e_rev = rel.use_rev, A.n_etab = rel.size;
+    if (nt.kind) A.ntab = nt.data, A.Pn = nt.P, A.rsn = nt.rs, A.sn = nt.s, A.n_ntab = nt.size;
     A.record = record;
     A.s_out = out.s;
     A.P_out = out.P;
@@ -497,6 +538,13 @@ struct CycleRunner {
     A.row_out = rows.as<uint64_t>();
     A.err = err;
     A.updates = upd;
+    static const bool dbg = std::getenv("MB_DEBUG_HOPS") != nullptr;
+    if (dbg)
+      fprintf(stderr, "hop n_in=%llu W=%llu s_in=%d P_in=%u first=%d in_r=%d out_r=%d rec=%d s_out=%d P_out=%u "
+              "etab=%p Pe=%u se=%d rse=%u erev=%d n_etab=%llu ntab=%p Pn=%u sn=%d rsn=%u bits=%d\n",
+              (unsigned long long)in.n, (unsigned long long)W, in.s, in.P, (int)first, in.has_r, out.has_r,
+              (int)record, out.s, out.P, (const void*)A.etab, A.Pe, A.se, A.rse, A.e_rev,
+              (unsigned long long)A.n_etab, (const void*)A.ntab, A.Pn, A.sn, A.rsn, bits);
     launch("cycle_hop_expand", [&] { k_hop_expand<<<grid_for(W, 256), 256, 0, stream>>>(A); });
     aggregate(keys, rows, W, out.P, out.key, out.pay, out.n);
     return true;
@@ -510,10 +558,13 @@ struct CycleRunner {
       r.off = walk_fwd_of_storage ? t.off : t.off_t;
       r.adj = walk_fwd_of_storage ? t.cols : t.cols_t;
       r.pay = walk_fwd_of_storage ? t.data : t.data_t;
+      r.size = walk_fwd_of_storage ? t.size : t.size_t_;
+      r.rs = t.P;
       r.P = t.P, r.s = t.s;
     } else {
       r.off = G.off, r.adj = G.adj;
-      if (t.kind == 3) r.pay = t.data, r.P = t.P, r.s = t.s, r.use_rev = !walk_fwd_of_storage;
+      if (t.kind == 3)
+        r.pay = t.data, r.P = t.P, r.rs = t.rs, r.s = t.s, r.use_rev = !walk_fwd_of_storage, r.size = t.size;
     }
     return r;
   }
@@ -533,7 +584,8 @@ struct CycleRunner {
     cur.pay.alloc(std::max<uint64_t>(static_cast<uint64_t>(nx) * cur.P, 1) * 8);
     launch("cycle_init", [&] {
       k_init_frontier<<<grid_for(nx, 256), 256, 0, stream>>>(x0, nx, bits, G.chi, use_start ? hn.data : nullptr,
-                                                             cur.P, cur.key.as<uint64_t>(), cur.pay.as<uint64_t>());
+                                                             cur.P, hn.rs, cur.key.as<uint64_t>(),
+                                                             cur.pay.as<uint64_t>());
     });
     int p = h;
     bool first = true;
@@ -599,7 +651,7 @@ struct CycleRunner {
     M.bits = bits;
     M.out_kind = C.out.kind == 1 ? 1 : (C.out.kind == 2 ? 2 : (C.out.kind == 3 ? 3 : 4));
     M.key_src0 = ks0, M.key_src1 = ks1;
-    M.out = C.out.data, M.Pout = C.out.P;
+    M.out = C.out.data, M.Pout = C.out.P, M.rso = C.out.rs;
     M.scalar = scalar, M.err = err, M.updates = upd;
     DBuf ck, cr;
     if (M.out_kind == 4) {

@@ -1,4 +1,4 @@
-// Leaf blocks, table-driven variant.  Included by engine.cu after its helpers.
+// Leaf blocks, table-driven and colouring-batched.  Included by engine.cu.
 //
 // Path-table extension along CSR rows (paper §5.2 leaf blocks; reference
 // engine.cpp:368-382: edge table -> node join on the leaf -> node join on the
@@ -6,9 +6,13 @@
 // side contributes, for every neighbour y, the row U_b[y] shifted by x's
 // colour.  Which output colour-set index an entry (colour of x, colour of y,
 // entry ib of U_b's row) lands in depends only on (chi x, chi y, ib), so the
-// whole colour-set arithmetic is precomputed into a shared-memory map and the
-// inner loop is: load neighbour id, its colour, its row (vectorised), and add
-// into the shared accumulator through the map.
+// colour-set arithmetic is precomputed into a shared-memory map and the inner
+// loop is: neighbour id, its colours, its rows, add through the map.
+//
+// Colouring batch: tables are laid out [row][colouring][entry] and colours
+// [vertex][8], so one pass over x's CSR row serves all C colourings of the
+// batch — the neighbour ids are read once and each neighbour's C rows are one
+// contiguous span.
 //
 // Degree-binned scheduling: a warp per light vertex, a 256-thread CTA per
 // heavy vertex (degree > 256), so hubs do not serialise a warp.
@@ -16,17 +20,17 @@
 struct LeafMapArgs {
   const uint64_t* off;
   const uint32_t* adj;
-  const uint8_t* chi;
+  const uint8_t* chi;  // [n][kChiStride], 0-based colours
   const uint64_t* ub;  // node child on the leaf (row = img b), may be null
   const uint64_t* ua;  // node child on the boundary (row = img a), may be null
   uint32_t Pb, Pa, PZ, Pout;
-  int sb, sa, sZ, k;
+  uint32_t rsb, rsa, rso;  // row strides (C_alloc * P)
+  int sb, sa, sZ, k, C;
   uint64_t* out;
   int* err;
   u64* updates;
 };
 
-// map entry for (cx, cy, ib): Z index, or 0xFFFF when chi x is in the leaf's set
 __device__ __forceinline__ uint32_t leaf_map_size(const LeafMapArgs& A) {
   return static_cast<uint32_t>(A.k) * A.k * (A.ub ? A.Pb : 1u);
 }
@@ -53,59 +57,67 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
   }
   __syncthreads();
   const int g = threadIdx.x / GROUP, lane = threadIdx.x % GROUP;
-  u64* Z = acc + static_cast<size_t>(g) * (A.PZ + A.Pout);
-  u64* O = Z + A.PZ;
+  const uint32_t gstride = A.C * (A.PZ + A.Pout);
+  u64* Z = acc + static_cast<size_t>(g) * gstride;  // [C][PZ] then [C][Pout]
+  u64* O = Z + A.C * A.PZ;
   uint64_t upd = 0;
   for (uint32_t gi = blockIdx.x * kGroups + g; gi < nv; gi += gridDim.x * kGroups) {
     const uint32_t x = vlist[gi];
-    for (uint32_t i = lane; i < A.PZ + A.Pout; i += GROUP) Z[i] = 0;
+    for (uint32_t i = lane; i < gstride; i += GROUP) Z[i] = 0;
     if (GROUP == 32) __syncwarp(); else __syncthreads();
-    const uint32_t cx = A.chi[x];
+    const uint64_t cxs = load_colors(A.chi, x);
     const uint64_t base = A.off[x], deg = A.off[x + 1] - base;
-    const uint16_t* mx = map + static_cast<size_t>(cx) * A.k * pb;
     for (uint64_t j = lane; j < deg; j += GROUP) {
       const uint32_t y = __ldg(A.adj + base + j);
-      const uint32_t cy = __ldg(A.chi + y);
-      const uint16_t* my = mx + cy * pb;
-      if (!A.ub) {
-        const uint16_t t = my[0];
-        if (t != 0xFFFF) {
-          atomicAdd(Z + t, 1ull);
+      const uint64_t cys = load_colors(A.chi, y);
+      const uint64_t* rowy = A.ub ? A.ub + static_cast<uint64_t>(y) * A.rsb : nullptr;
+      for (int c = 0; c < A.C; ++c) {
+        const uint32_t cx = color_of(cxs, c), cy = color_of(cys, c);
+        const uint16_t* my = map + (cx * A.k + cy) * pb;
+        u64* Zc = Z + c * A.PZ;
+        if (!A.ub) {
+          const uint16_t t = my[0];
+          if (t != 0xFFFF) {
+            atomicAdd(Zc + t, 1ull);
+            ++upd;
+          }
+          continue;
+        }
+        if (cy == cx) continue;
+        const uint64_t* row = rowy + c * pb;
+        for (uint32_t ib = 0; ib < pb; ++ib) {
+          const uint64_t v = __ldg(row + ib);
+          if (!v) continue;
+          const uint16_t t = my[ib];
+          if (t == 0xFFFF) continue;
+          atomic_add_ck(Zc + t, v, A.err);
           ++upd;
         }
-        continue;
-      }
-      if (cy == cx) continue;
-      const uint64_t* row = A.ub + static_cast<uint64_t>(y) * pb;
-      for (uint32_t ib = 0; ib < pb; ++ib) {
-        const uint64_t v = __ldg(row + ib);
-        if (!v) continue;
-        const uint16_t t = my[ib];
-        if (t == 0xFFFF) continue;
-        atomic_add_ck(Z + t, v, A.err);
-        ++upd;
       }
     }
     if (GROUP == 32) __syncwarp(); else __syncthreads();
+    uint64_t* orow = A.out + static_cast<uint64_t>(x) * A.rso;
     if (!A.ua) {
-      for (uint32_t i = lane; i < A.Pout; i += GROUP) A.out[static_cast<uint64_t>(x) * A.Pout + i] = Z[i];
+      for (uint32_t i = lane; i < A.C * A.Pout; i += GROUP) orow[i] = Z[i];
     } else {
-      const uint32_t fx = 1u << cx;
-      const uint64_t items = static_cast<uint64_t>(A.PZ) * A.Pa;
-      for (uint64_t it = lane; it < items; it += GROUP) {
-        const uint32_t iz = static_cast<uint32_t>(it / A.Pa), ia = static_cast<uint32_t>(it - iz * A.Pa);
-        const uint64_t z = Z[iz];
+      const uint64_t per = static_cast<uint64_t>(A.PZ) * A.Pa;
+      for (uint64_t it = lane; it < per * A.C; it += GROUP) {
+        const int c = static_cast<int>(it / per);
+        const uint64_t r = it - c * per;
+        const uint32_t iz = static_cast<uint32_t>(r / A.Pa), ia = static_cast<uint32_t>(r - iz * A.Pa);
+        const uint64_t z = Z[c * A.PZ + iz];
         if (!z) continue;
-        const uint64_t a = __ldg(A.ua + static_cast<uint64_t>(x) * A.Pa + ia);
+        const uint64_t a = __ldg(A.ua + static_cast<uint64_t>(x) * A.rsa + c * A.Pa + ia);
         if (!a) continue;
+        const uint32_t fx = 1u << color_of(cxs, c);
         const uint32_t Mz = sig_expand(sig_unrank(c_lut, A.sZ - 1, iz), fx);
         const uint32_t Ma = sig_expand(sig_unrank(c_lut, A.sa - 1, ia), fx);
         if ((Mz & Ma) != fx) continue;
-        atomic_add_ck(O + sig_index(c_lut, Mz | Ma, fx), mul_ck(z, a, A.err), A.err);
+        atomic_add_ck(O + c * A.Pout + sig_index(c_lut, Mz | Ma, fx), mul_ck(z, a, A.err), A.err);
         ++upd;
       }
       if (GROUP == 32) __syncwarp(); else __syncthreads();
-      for (uint32_t i = lane; i < A.Pout; i += GROUP) A.out[static_cast<uint64_t>(x) * A.Pout + i] = O[i];
+      for (uint32_t i = lane; i < A.C * A.Pout; i += GROUP) orow[i] = O[i];
     }
     if (GROUP == 32) __syncwarp(); else __syncthreads();
   }
