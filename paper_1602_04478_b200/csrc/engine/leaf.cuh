@@ -58,12 +58,17 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
   __syncthreads();
   const int g = threadIdx.x / GROUP, lane = threadIdx.x % GROUP;
   const uint32_t gstride = A.C * (A.PZ + A.Pout);
-  u64* Z = acc + static_cast<size_t>(g) * gstride;  // [C][PZ] then [C][Pout]
+  // a CTA-sized group keeps one accumulator copy per warp (no cross-warp
+  // contention on the same counters) and sums the copies at the end
+  constexpr int kWarpsPerGroup = GROUP / 32;
+  u64* Zg = acc + static_cast<size_t>(g) * gstride * kWarpsPerGroup;
+  u64* Z = Zg;                      // [C][PZ] then [C][Pout]: the reduced copy
+  u64* Zw = Zg + (lane / 32) * gstride;  // this warp's copy
   u64* O = Z + A.C * A.PZ;
   uint64_t upd = 0;
   for (uint32_t gi = blockIdx.x * kGroups + g; gi < nv; gi += gridDim.x * kGroups) {
     const uint32_t x = vlist[gi];
-    for (uint32_t i = lane; i < gstride; i += GROUP) Z[i] = 0;
+    for (uint32_t i = lane; i < gstride * kWarpsPerGroup; i += GROUP) Zg[i] = 0;
     if (GROUP == 32) __syncwarp(); else __syncthreads();
     const uint64_t cxs = load_colors(A.chi, x);
     const uint64_t base = A.off[x], deg = A.off[x + 1] - base;
@@ -74,7 +79,7 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
       for (int c = 0; c < A.C; ++c) {
         const uint32_t cx = color_of(cxs, c), cy = color_of(cys, c);
         const uint16_t* my = map + (cx * A.k + cy) * pb;
-        u64* Zc = Z + c * A.PZ;
+        u64* Zc = Zw + c * A.PZ;
         if (!A.ub) {
           const uint16_t t = my[0];
           if (t != 0xFFFF) {
@@ -95,7 +100,17 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
         }
       }
     }
-    if (GROUP == 32) __syncwarp(); else __syncthreads();
+    if (GROUP == 32) {
+      __syncwarp();
+    } else {
+      __syncthreads();
+      for (uint32_t i = lane; i < A.C * A.PZ; i += GROUP) {
+        uint64_t s = Zg[i];
+        for (int w = 1; w < kWarpsPerGroup; ++w) s = add_ck(s, Zg[w * gstride + i], A.err);
+        Z[i] = s;
+      }
+      __syncthreads();
+    }
     uint64_t* orow = A.out + static_cast<uint64_t>(x) * A.rso;
     if (!A.ua) {
       for (uint32_t i = lane; i < A.C * A.Pout; i += GROUP) orow[i] = Z[i];
