@@ -320,6 +320,17 @@ unsigned grid_for(uint64_t work, unsigned block) {
   return static_cast<unsigned>(std::max<uint64_t>(1, g));
 }
 
+// Sort keys for the CN-length edge order: ~length so an ascending sort yields
+// decreasing lengths.
+__global__ void k_cn_len_keys(const uint64_t* __restrict__ cn_off, uint64_t nout, uint32_t* __restrict__ keys,
+                              uint32_t* __restrict__ vals) {
+  const uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (j >= nout) return;
+  const uint64_t len = cn_off[j + 1] - cn_off[j];
+  keys[j] = ~static_cast<uint32_t>(len > 0xFFFFFFFFull ? 0xFFFFFFFFull : len);
+  vals[j] = static_cast<uint32_t>(j);
+}
+
 __global__ void k_gather_u32(const uint32_t* __restrict__ idx, const uint32_t* __restrict__ src,
                              uint32_t* __restrict__ out, uint64_t count) {
   const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;

@@ -296,6 +296,8 @@ struct TriHistArgs {
   const uint32_t* rev;
   const uint8_t* chi;   // [n][kChiStride]
   int k, C;
+  int lane_mode;            // 1: lane per edge, register counters (k <= 8, lists < 65536)
+  const uint32_t* eorder;   // oriented edges in CN-length order (lane_mode)
   // stage 1: this block
   int s_out;
   uint32_t P2;          // C(k-2, s_out-2): entries of S containing both pivot colours
@@ -331,7 +333,7 @@ __host__ __device__ inline HistSmem hist_smem_layout(int k, int C, uint32_t P2, 
   L.i1 = out_kind == 1 ? (kk * P2 + 1) / 2 : 0;                 // u16 pairs as u32
   L.t2 = out_kind == 3 ? kk * P2p * ntermp : 0;                 // u32
   L.i2 = (out_kind == 3 && pout_kind == 1) ? (kk * P2p + 1) / 2 : 0;
-  L.hist_per_warp = 32u * C * k;                                // u32
+  L.hist_per_warp = 32u * (C * k + 1);                          // u32, odd per-edge stride
   L.tbuf_per_warp = out_kind == 3 ? 32u * 2 * P2 * 2 : 0;       // u64 as 2 u32
   return L;
 }
@@ -362,7 +364,7 @@ __device__ __forceinline__ void build_terms(uint32_t* terms, uint16_t* idx1, int
   }
 }
 
-__global__ void __launch_bounds__(32 * kHistWarps) tri_hist_kernel(TriHistArgs A) {
+__global__ void __launch_bounds__(32 * kHistWarps, 3) tri_hist_kernel(TriHistArgs A) {
   extern __shared__ uint32_t hsm[];
   const int k = A.k, C = A.C;
   const HistSmem L = hist_smem_layout(k, C, A.P2, A.nterm, A.out_kind, A.P2p, A.ntermp, A.pout_kind);
@@ -381,39 +383,85 @@ __global__ void __launch_bounds__(32 * kHistWarps) tri_hist_kernel(TriHistArgs A
 #pragma unroll
   for (int c = 0; c < kChiStride; ++c) local[c] = 0;
   uint64_t upd = 0;
+  const uint32_t LS = static_cast<uint32_t>(C) * k + 1;  // per-edge row of counters (odd: no bank conflicts)
   const uint64_t nbatch = (A.nout + 31) / 32;
   for (uint64_t bt = static_cast<uint64_t>(blockIdx.x) * kHistWarps + wid; bt < nbatch;
        bt += static_cast<uint64_t>(gridDim.x) * kHistWarps) {
     const uint64_t j0 = bt * 32;
-    const uint64_t j = j0 + lane;
-    const bool live = j < A.nout;
-    for (uint32_t i = lane; i < L.hist_per_warp; i += 32) hist[i] = 0;
-    const uint64_t myoff = A.cn_off[live ? j : A.nout];
-    const uint64_t endoff = A.cn_off[min(j0 + 32, A.nout)];
-    const uint64_t startoff = __shfl_sync(0xffffffffu, myoff, 0);
-    __syncwarp();
-    for (uint64_t e0 = startoff; e0 < endoff; e0 += 32) {
-      const uint64_t e = e0 + lane;
-      int lo = 0;
+    const bool live = j0 + lane < A.nout;
+    uint64_t j = j0 + lane;
+    if (A.lane_mode) {
+      // lane owns one oriented edge (edges visited in CN-length order, so the
+      // 32 lists of a warp have similar lengths) and counts its common
+      // neighbours' colours for all C colourings in registers: 16-bit fields,
+      // four colours per word.  No shared-memory atomics; the list is read
+      // with 16-byte loads.
+      if (live) j = A.eorder[j];
+      uint64_t H[kChiStride][2];
 #pragma unroll
-      for (int step = 16; step > 0; step >>= 1) {
-        const uint64_t o = __shfl_sync(0xffffffffu, myoff, lo + step);
-        if (o <= e) lo += step;
+      for (int c = 0; c < kChiStride; ++c) H[c][0] = H[c][1] = 0;
+      if (live) {
+        const uint64_t lo_ = A.cn_off[j], hi_ = A.cn_off[j + 1];
+        for (uint64_t p = lo_ & ~3ull; p < hi_; p += 4) {
+          const uint4 q = __ldg(reinterpret_cast<const uint4*>(A.cn_w + p));
+          const uint32_t ws[4] = {q.x, q.y, q.z, q.w};
+          uint64_t cw[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const bool in = p + u >= lo_ && p + u < hi_;
+            cw[u] = in ? load_colors(A.chi, ws[u]) : ~0ull;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            if (cw[u] == ~0ull) continue;
+#pragma unroll
+            for (int c = 0; c < kChiStride; ++c) {
+              const uint32_t d = color_of(cw[u], c);
+              const uint64_t inc = 1ull << (16 * (d & 3));
+              if (d < 4) H[c][0] += inc; else H[c][1] += inc;
+            }
+          }
+        }
       }
-      if (e < endoff) {
-        const uint32_t w = __ldg(A.cn_w + e);
-        const uint64_t cw = load_colors(A.chi, w);
-        uint32_t* h = hist + lo * C * k;
-        for (int c = 0; c < C; ++c) atomicAdd(h + c * k + color_of(cw, c), 1u);
+      uint32_t* hrow = hist + lane * LS;
+#pragma unroll
+      for (int c = 0; c < kChiStride; ++c) {
+        if (c < C) {
+#pragma unroll
+          for (int d = 0; d < 8; ++d)  // static indices keep H in registers
+            if (d < k) hrow[c * k + d] = static_cast<uint32_t>((H[c][d >> 2] >> (16 * (d & 3))) & 0xFFFFu);
+        }
       }
+      __syncwarp();
+    } else {
+      for (uint32_t i = lane; i < L.hist_per_warp; i += 32) hist[i] = 0;
+      const uint64_t myoff = A.cn_off[live ? j : A.nout];
+      const uint64_t endoff = A.cn_off[min(j0 + 32, A.nout)];
+      const uint64_t startoff = __shfl_sync(0xffffffffu, myoff, 0);
+      __syncwarp();
+      for (uint64_t e0 = startoff; e0 < endoff; e0 += 32) {
+        const uint64_t e = e0 + lane;
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1) {
+          const uint64_t o = __shfl_sync(0xffffffffu, myoff, lo + step);
+          if (o <= e) lo += step;
+        }
+        if (e < endoff) {
+          const uint32_t w = __ldg(A.cn_w + e);
+          const uint64_t cw = load_colors(A.chi, w);
+          uint32_t* h = hist + lo * LS;
+          for (int c = 0; c < C; ++c) atomicAdd(h + c * k + color_of(cw, c), 1u);
+        }
+      }
+      __syncwarp();
     }
-    __syncwarp();
     if (live) {
       const uint32_t a = A.out_src[j], b = A.out_nbr[j];
       const uint32_t sab = A.out_slot[j], sba = A.rev[sab];
       const uint64_t cas = load_colors(A.chi, a), cbs = load_colors(A.chi, b);
       for (int c = 0; c < C; ++c) {
-        const uint32_t* h = hist + (lane * C + c) * k;
+        const uint32_t* h = hist + lane * LS + c * k;
         const uint32_t ca = color_of(cas, c), cb = color_of(cbs, c);
         uint64_t acc = 0;
         for (int o = 0; o < 2; ++o) {
