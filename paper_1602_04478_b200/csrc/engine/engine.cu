@@ -12,6 +12,7 @@
 #include <map>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../host/errors.hpp"
@@ -151,14 +152,15 @@ __global__ void k_reverse_slots(uint64_t m2, const uint64_t* __restrict__ off,
 // Colourings c0..c0+C-1 (row-major [colouring][vertex], colours 1..k) into the
 // interleaved 0-based layout [vertex][kChiStride]; unused slots are zeroed.
 __global__ void k_recolor(uint32_t n, int C, const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int k,
-                          int* err) {
+                          int* err, const uint32_t* __restrict__ order) {
   const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= n) return;
+  const uint32_t src = order[v];  // caller's id of device vertex v
   unsigned long long cols = 0;
 #pragma unroll
   for (int c = 0; c < kChiStride; ++c) {
     if (c < C) {
-      const int cc = in[static_cast<uint64_t>(c) * n + v];
+      const int cc = in[static_cast<uint64_t>(c) * n + src];
       if (cc < 1 || cc > k) atomicOr(err, 2);
       cols |= static_cast<unsigned long long>((cc - 1) & 0xFF) << (8 * c);
     }
