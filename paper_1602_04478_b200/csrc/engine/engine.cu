@@ -325,10 +325,12 @@ unsigned grid_for(uint64_t work, unsigned block) {
 // Sort keys for the CN-length edge order: ~length so an ascending sort yields
 // decreasing lengths.
 __global__ void k_cn_len_keys(const uint64_t* __restrict__ cn_off, uint64_t nout, uint32_t* __restrict__ keys,
-                              uint32_t* __restrict__ vals) {
+                              uint32_t* __restrict__ vals, u64* __restrict__ nonempty) {
   const uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const uint64_t len = j < nout ? cn_off[j + 1] - cn_off[j] : 0;
+  const unsigned nz = __ballot_sync(0xffffffffu, len > 0);
+  if ((threadIdx.x & 31) == 0 && nz) atomicAdd(nonempty, static_cast<u64>(__popc(nz)));
   if (j >= nout) return;
-  const uint64_t len = cn_off[j + 1] - cn_off[j];
   keys[j] = ~static_cast<uint32_t>(len > 0xFFFFFFFFull ? 0xFFFFFFFFull : len);
   vals[j] = static_cast<uint32_t>(j);
 }

@@ -71,33 +71,35 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
     for (uint32_t i = lane; i < gstride * kWarpsPerGroup; i += GROUP) Zg[i] = 0;
     if (GROUP == 32) __syncwarp(); else __syncthreads();
     const uint64_t cxs = load_colors(A.chi, x);
-    const uint64_t base = A.off[x], deg = A.off[x + 1] - base;
-    for (uint64_t j = lane; j < deg; j += GROUP) {
+    const uint64_t base = A.off[x];
+    const uint32_t deg = static_cast<uint32_t>(A.off[x + 1] - base);
+    // one lane per (neighbour, colouring): low-degree rows still fill the
+    // warp, and a neighbour's C rows are read as one contiguous span
+    const uint32_t items = deg * static_cast<uint32_t>(A.C);
+    for (uint32_t it = lane; it < items; it += GROUP) {
+      const uint32_t j = it / static_cast<uint32_t>(A.C);
+      const int c = static_cast<int>(it - j * static_cast<uint32_t>(A.C));
       const uint32_t y = __ldg(A.adj + base + j);
-      const uint64_t cys = load_colors(A.chi, y);
-      const uint64_t* rowy = A.ub ? A.ub + static_cast<uint64_t>(y) * A.rsb : nullptr;
-      for (int c = 0; c < A.C; ++c) {
-        const uint32_t cx = color_of(cxs, c), cy = color_of(cys, c);
-        const uint16_t* my = map + (cx * A.k + cy) * pb;
-        u64* Zc = Zw + c * A.PZ;
-        if (!A.ub) {
-          const uint16_t t = my[0];
-          if (t != 0xFFFF) {
-            atomicAdd(Zc + t, 1ull);
-            ++upd;
-          }
-          continue;
-        }
-        if (cy == cx) continue;
-        const uint64_t* row = rowy + c * pb;
-        for (uint32_t ib = 0; ib < pb; ++ib) {
-          const uint64_t v = __ldg(row + ib);
-          if (!v) continue;
-          const uint16_t t = my[ib];
-          if (t == 0xFFFF) continue;
-          atomic_add_ck(Zc + t, v, A.err);
+      const uint32_t cx = color_of(cxs, c), cy = A.chi[static_cast<uint64_t>(y) * kChiStride + c];
+      const uint16_t* my = map + (cx * A.k + cy) * pb;
+      u64* Zc = Zw + c * A.PZ;
+      if (!A.ub) {
+        const uint16_t t = my[0];
+        if (t != 0xFFFF) {
+          atomicAdd(Zc + t, 1ull);
           ++upd;
         }
+        continue;
+      }
+      if (cy == cx) continue;
+      const uint64_t* row = A.ub + static_cast<uint64_t>(y) * A.rsb + c * pb;
+      for (uint32_t ib = 0; ib < pb; ++ib) {
+        const uint64_t v = __ldg(row + ib);
+        if (!v) continue;
+        const uint16_t t = my[ib];
+        if (t == 0xFFFF) continue;
+        atomic_add_ck(Zc + t, v, A.err);
+        ++upd;
       }
     }
     if (GROUP == 32) {

@@ -288,6 +288,7 @@ __global__ void __launch_bounds__(32 * kTriWarps) tri_edge_block_kernel(TriEdgeA
 
 struct TriHistArgs {
   uint64_t nout;
+  uint64_t nitems;  // edges visited: nout, or in lane mode the non-empty prefix of eorder
   const uint64_t* cn_off;
   const uint32_t* cn_w;
   const uint32_t* out_src;
@@ -334,7 +335,7 @@ __host__ __device__ inline HistSmem hist_smem_layout(int k, int C, uint32_t P2, 
   L.t2 = out_kind == 3 ? kk * P2p * ntermp : 0;                 // u32
   L.i2 = (out_kind == 3 && pout_kind == 1) ? (kk * P2p + 1) / 2 : 0;
   L.hist_per_warp = 32u * (C * k + 1);                          // u32, odd per-edge stride
-  L.tbuf_per_warp = out_kind == 3 ? 32u * 2 * P2 * 2 : 0;       // u64 as 2 u32
+  L.tbuf_per_warp = out_kind == 3 ? 32u * (2 * P2 + 1) * 2 : 0;  // u64 as 2 u32, odd per-lane stride
   return L;
 }
 
@@ -378,17 +379,17 @@ __global__ void __launch_bounds__(32 * kHistWarps, 3) tri_hist_kernel(TriHistArg
   __syncthreads();
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t* hist = wbase + static_cast<size_t>(wid) * (L.hist_per_warp + L.tbuf_per_warp);
-  u64* tbuf = reinterpret_cast<u64*>(hist + L.hist_per_warp) + static_cast<size_t>(lane) * 2 * A.P2;
+  u64* tbuf = reinterpret_cast<u64*>(hist + L.hist_per_warp) + static_cast<size_t>(lane) * (2 * A.P2 + 1);
   uint64_t local[kChiStride];
 #pragma unroll
   for (int c = 0; c < kChiStride; ++c) local[c] = 0;
   uint64_t upd = 0;
   const uint32_t LS = static_cast<uint32_t>(C) * k + 1;  // per-edge row of counters (odd: no bank conflicts)
-  const uint64_t nbatch = (A.nout + 31) / 32;
+  const uint64_t nbatch = (A.nitems + 31) / 32;
   for (uint64_t bt = static_cast<uint64_t>(blockIdx.x) * kHistWarps + wid; bt < nbatch;
        bt += static_cast<uint64_t>(gridDim.x) * kHistWarps) {
     const uint64_t j0 = bt * 32;
-    const bool live = j0 + lane < A.nout;
+    const bool live = j0 + lane < A.nitems;
     uint64_t j = j0 + lane;
     if (A.lane_mode) {
       // lane owns one oriented edge (edges visited in CN-length order, so the
