@@ -322,20 +322,30 @@ struct TriHistArgs {
 
 constexpr int kHistWarps = 8;
 
+// per-edge histogram row in u32 words: u16 counters in lane mode (lists are
+// shorter than 65536 there), u32 in flat mode (shared-memory atomics); odd
+// so the 32 rows of a warp fall in distinct banks
+__host__ __device__ inline uint32_t hist_lane_words(int C, int k, int lane_mode) {
+  const uint32_t n = static_cast<uint32_t>(C) * k;
+  return lane_mode ? ((n + 1) / 2) | 1u : n + 1;
+}
+
 struct HistSmem {  // shared-memory carve-up (host computes the same sizes)
-  uint32_t t1, i1, t2, i2, hist_per_warp, tbuf_per_warp;
+  uint32_t t1, i1, t2, i2, hist_per_warp, tbuf_per_warp, fst_per_warp;
 };
 
 __host__ __device__ inline HistSmem hist_smem_layout(int k, int C, uint32_t P2, int nterm, int out_kind,
-                                                     uint32_t P2p, int ntermp, int pout_kind) {
+                                                     uint32_t P2p, int ntermp, int pout_kind, uint32_t PF,
+                                                     int lane_mode) {
   HistSmem L;
   const uint32_t kk = static_cast<uint32_t>(k) * k;
   L.t1 = kk * P2 * nterm;                                       // u32
   L.i1 = out_kind == 1 ? (kk * P2 + 1) / 2 : 0;                 // u16 pairs as u32
   L.t2 = out_kind == 3 ? kk * P2p * ntermp : 0;                 // u32
   L.i2 = (out_kind == 3 && pout_kind == 1) ? (kk * P2p + 1) / 2 : 0;
-  L.hist_per_warp = 32u * (C * k + 1);                          // u32, odd per-edge stride
+  L.hist_per_warp = 32u * hist_lane_words(C, k, lane_mode);    // u32, odd per-edge stride
   L.tbuf_per_warp = out_kind == 3 ? 32u * (2 * P2 + 1) * 2 : 0;  // u64 as 2 u32, odd per-lane stride
+  L.fst_per_warp = PF ? 32u * (PF | 1u) * 2 : 0;                  // staged factor row (u64), odd stride
   return L;
 }
 
@@ -368,7 +378,9 @@ __device__ __forceinline__ void build_terms(uint32_t* terms, uint16_t* idx1, int
 __global__ void __launch_bounds__(32 * kHistWarps, 3) tri_hist_kernel(TriHistArgs A) {
   extern __shared__ uint32_t hsm[];
   const int k = A.k, C = A.C;
-  const HistSmem L = hist_smem_layout(k, C, A.P2, A.nterm, A.out_kind, A.P2p, A.ntermp, A.pout_kind);
+  const uint32_t PF = A.fkind ? A.PF : 0u;
+  const HistSmem L = hist_smem_layout(k, C, A.P2, A.nterm, A.out_kind, A.P2p, A.ntermp, A.pout_kind, PF,
+                                      A.lane_mode);
   uint32_t* terms = hsm;
   uint16_t* idx1 = reinterpret_cast<uint16_t*>(hsm + L.t1);
   uint32_t* termsp = hsm + L.t1 + L.i1;
@@ -378,13 +390,17 @@ __global__ void __launch_bounds__(32 * kHistWarps, 3) tri_hist_kernel(TriHistArg
   if (A.out_kind == 3) build_terms(termsp, idx1p, k, A.P2p, A.s_out + 1, A.ntermp, 3, A.pout_kind == 1);
   __syncthreads();
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  uint32_t* hist = wbase + static_cast<size_t>(wid) * (L.hist_per_warp + L.tbuf_per_warp);
+  uint32_t* hist = wbase + static_cast<size_t>(wid) * (L.hist_per_warp + L.tbuf_per_warp + L.fst_per_warp);
   u64* tbuf = reinterpret_cast<u64*>(hist + L.hist_per_warp) + static_cast<size_t>(lane) * (2 * A.P2 + 1);
+  u64* fst = reinterpret_cast<u64*>(hist + L.hist_per_warp + L.tbuf_per_warp) + static_cast<size_t>(lane) * (PF | 1u);
+  uint16_t* hist16 = reinterpret_cast<uint16_t*>(hist);
+  uint32_t ovf = 0;  // overflow seen by this thread (one atomic at exit)
   uint64_t local[kChiStride];
 #pragma unroll
   for (int c = 0; c < kChiStride; ++c) local[c] = 0;
   uint64_t upd = 0;
-  const uint32_t LS = static_cast<uint32_t>(C) * k + 1;  // per-edge row of counters (odd: no bank conflicts)
+  const uint32_t LSW = hist_lane_words(C, k, A.lane_mode);
+  const uint32_t LS = A.lane_mode ? 2 * LSW : LSW;  // per-edge row stride in counters
   const uint64_t nbatch = (A.nitems + 31) / 32;
   for (uint64_t bt = static_cast<uint64_t>(blockIdx.x) * kHistWarps + wid; bt < nbatch;
        bt += static_cast<uint64_t>(gridDim.x) * kHistWarps) {
@@ -424,13 +440,13 @@ __global__ void __launch_bounds__(32 * kHistWarps, 3) tri_hist_kernel(TriHistArg
           }
         }
       }
-      uint32_t* hrow = hist + lane * LS;
+      uint16_t* hrow = hist16 + lane * LS;
 #pragma unroll
       for (int c = 0; c < kChiStride; ++c) {
         if (c < C) {
 #pragma unroll
           for (int d = 0; d < 8; ++d)  // static indices keep H in registers
-            if (d < k) hrow[c * k + d] = static_cast<uint32_t>((H[c][d >> 2] >> (16 * (d & 3))) & 0xFFFFu);
+            if (d < k) hrow[c * k + d] = static_cast<uint16_t>(H[c][d >> 2] >> (16 * (d & 3)));
         }
       }
       __syncwarp();
@@ -462,7 +478,8 @@ __global__ void __launch_bounds__(32 * kHistWarps, 3) tri_hist_kernel(TriHistArg
       const uint32_t sab = A.out_slot[j], sba = A.rev[sab];
       const uint64_t cas = load_colors(A.chi, a), cbs = load_colors(A.chi, b);
       for (int c = 0; c < C; ++c) {
-        const uint32_t* h = hist + lane * LS + c * k;
+        const uint32_t hb = lane * LS + c * k;
+        auto hval = [&](uint32_t d) -> uint32_t { return A.lane_mode ? hist16[hb + d] : hist[hb + d]; };
         const uint32_t ca = color_of(cas, c), cb = color_of(cbs, c);
         uint64_t acc = 0;
         for (int o = 0; o < 2; ++o) {
@@ -475,11 +492,23 @@ __global__ void __launch_bounds__(32 * kHistWarps, 3) tri_hist_kernel(TriHistArg
               for (uint32_t i = 0; i < A.P2; ++i) tbuf[o * A.P2 + i] = 0;
             continue;
           }
-          const uint64_t* F = nullptr;
-          if (A.fkind == 1) F = A.F + static_cast<uint64_t>(o ? b : a) * A.rsF + c * A.PF;
-          else if (A.fkind == 2) F = A.F + static_cast<uint64_t>(o ? a : b) * A.rsF + c * A.PF;
-          else if (A.fkind == 3)
-            F = A.F + static_cast<uint64_t>((o == 0) != (A.sw01 != 0) ? sab : sba) * A.rsF + c * A.PF;
+          if (PF) {
+            // stage this orientation's factor row: independent loads in
+            // flight together instead of one dependent gather per term
+            const uint64_t* F;
+            if (A.fkind == 1) F = A.F + static_cast<uint64_t>(o ? b : a) * A.rsF + c * A.PF;
+            else if (A.fkind == 2) F = A.F + static_cast<uint64_t>(o ? a : b) * A.rsF + c * A.PF;
+            else F = A.F + static_cast<uint64_t>((o == 0) != (A.sw01 != 0) ? sab : sba) * A.rsF + c * A.PF;
+            for (uint32_t i0 = 0; i0 < PF; i0 += 8) {
+              uint64_t r[8];
+#pragma unroll
+              for (int u = 0; u < 8; ++u) r[u] = i0 + u < PF ? __ldg(F + i0 + u) : 0ull;
+#pragma unroll
+              for (int u = 0; u < 8; ++u)
+                if (i0 + u < PF) fst[i0 + u] = r[u];
+            }
+          }
+          const u64* Fs = PF ? fst : nullptr;
           const uint32_t tb = (c0 * k + c1) * A.P2;
           for (uint32_t i = 0; i < A.P2; ++i) {
             const uint32_t* tt = terms + static_cast<size_t>(tb + i) * A.nterm;
@@ -487,11 +516,14 @@ __global__ void __launch_bounds__(32 * kHistWarps, 3) tri_hist_kernel(TriHistArg
             for (int t = 0; t < A.nterm; ++t) {
               const uint32_t x = tt[t];
               if (x == ~0u) continue;
-              const uint32_t hc = h[x >> 16];
+              const uint32_t hc = hval(x >> 16);
               if (!hc) continue;
-              const uint64_t f = F ? __ldg(F + (x & 0xFFFFu)) : 1ull;
+              const uint64_t f = Fs ? Fs[x & 0xFFFFu] : 1ull;
               if (!f) continue;
-              v = add_ck(v, mul_ck(f, hc, A.err), A.err);
+              ovf |= __umul64hi(f, hc) != 0;
+              const uint64_t fh = f * hc;
+              v += fh;
+              ovf |= v < fh;
               ++upd;
             }
             if (A.out_kind == 2) {
@@ -500,7 +532,10 @@ __global__ void __launch_bounds__(32 * kHistWarps, 3) tri_hist_kernel(TriHistArg
               tbuf[o * A.P2 + i] = v;
             } else if (v) {
               if (A.out_kind == 0)
-                acc = add_ck(acc, v, A.err);
+                {
+                  acc += v;
+                  ovf |= acc < v;
+                }
               else
                 atomic_add_ck(reinterpret_cast<u64*>(A.out) + static_cast<uint64_t>(o ? b : a) * A.rso + c * A.Pout +
                                   idx1[tb + i], v, A.err);
@@ -521,18 +556,24 @@ __global__ void __launch_bounds__(32 * kHistWarps, 3) tri_hist_kernel(TriHistArg
               for (int t = 0; t < A.ntermp; ++t) {
                 const uint32_t x = tt[t];
                 if (x == ~0u) continue;
-                const uint32_t hc = h[x >> 16];
+                const uint32_t hc = hval(x >> 16);
                 if (!hc) continue;
                 const uint64_t f = T[x & 0xFFFFu];
                 if (!f) continue;
-                v = add_ck(v, mul_ck(f, hc, A.err), A.err);
+                ovf |= __umul64hi(f, hc) != 0;
+                const uint64_t fh = f * hc;
+                v += fh;
+                ovf |= v < fh;
                 ++upd;
               }
               if (A.pout_kind == 2) {
                 A.pout[static_cast<uint64_t>(o ? sba : sab) * A.rsop + c * A.Poutp + i] = v;
               } else if (v) {
                 if (A.pout_kind == 0)
-                  acc = add_ck(acc, v, A.err);
+                  {
+                  acc += v;
+                  ovf |= acc < v;
+                }
                 else
                   atomic_add_ck(reinterpret_cast<u64*>(A.pout) + static_cast<uint64_t>(o ? b : a) * A.rsop +
                                     c * A.Poutp + idx1p[tb + i], v, A.err);
@@ -546,7 +587,10 @@ __global__ void __launch_bounds__(32 * kHistWarps, 3) tri_hist_kernel(TriHistArg
         }
 #pragma unroll
         for (int cc = 0; cc < kChiStride; ++cc)
-          if (cc == c) local[cc] = add_ck(local[cc], acc, A.err);
+          if (cc == c) {
+            local[cc] += acc;
+            ovf |= local[cc] < acc;
+          }
       }
     }
     __syncwarp();
@@ -560,6 +604,7 @@ __global__ void __launch_bounds__(32 * kHistWarps, 3) tri_hist_kernel(TriHistArg
       if (lane == 0 && v) atomic_add_ck(A.scalars + c, v, A.err);
     }
   }
+  if (ovf) atomicOr(A.err, 1);
   for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(0xffffffffu, upd, o);
   if (lane == 0 && upd) atomicAdd(A.updates, static_cast<u64>(upd));
 }
