@@ -410,15 +410,30 @@ __global__ void __launch_bounds__(32 * kHistWarps, 3) tri_hist_kernel(TriHistArg
     if (A.lane_mode) {
       // lane owns one oriented edge (edges visited in CN-length order, so the
       // 32 lists of a warp have similar lengths) and counts its common
-      // neighbours' colours for all C colourings in registers: 16-bit fields,
-      // four colours per word.  No shared-memory atomics; the list is read
-      // with 16-byte loads.
+      // neighbours' colours for all C colourings in registers: 4-bit fields
+      // (k <= 8 colours in one word) flushed every 12 entries into 16-bit
+      // fields (two colours per word).  No shared-memory atomics; the list is
+      // read with 16-byte loads.
       if (live) j = A.eorder[j];
-      uint64_t H[kChiStride][2];
+      uint32_t N[kChiStride], H[kChiStride][4];
 #pragma unroll
-      for (int c = 0; c < kChiStride; ++c) H[c][0] = H[c][1] = 0;
+      for (int c = 0; c < kChiStride; ++c) {
+        N[c] = 0;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) H[c][w] = 0;
+      }
+      auto flush = [&]() {
+#pragma unroll
+        for (int c = 0; c < kChiStride; ++c) {
+          const uint32_t ev = N[c] & 0x0F0F0F0Fu, od = (N[c] >> 4) & 0x0F0F0F0Fu;
+#pragma unroll
+          for (int w = 0; w < 4; ++w) H[c][w] += ((ev >> (8 * w)) & 0xFFu) | (((od >> (8 * w)) & 0xFFu) << 16);
+          N[c] = 0;
+        }
+      };
       if (live) {
         const uint64_t lo_ = A.cn_off[j], hi_ = A.cn_off[j + 1];
+        int pend = 0;
         for (uint64_t p = lo_ & ~3ull; p < hi_; p += 4) {
           const uint4 q = __ldg(reinterpret_cast<const uint4*>(A.cn_w + p));
           const uint32_t ws[4] = {q.x, q.y, q.z, q.w};
@@ -431,14 +446,19 @@ __global__ void __launch_bounds__(32 * kHistWarps, 3) tri_hist_kernel(TriHistArg
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             if (cw[u] == ~0ull) continue;
+            const uint32_t lo32 = static_cast<uint32_t>(cw[u]), hi32 = static_cast<uint32_t>(cw[u] >> 32);
 #pragma unroll
             for (int c = 0; c < kChiStride; ++c) {
-              const uint32_t d = color_of(cw[u], c);
-              const uint64_t inc = 1ull << (16 * (d & 3));
-              if (d < 4) H[c][0] += inc; else H[c][1] += inc;
+              const uint32_t half = c < 4 ? lo32 : hi32;
+              N[c] += 1u << (((half >> (8 * (c & 3))) & 7u) << 2);
             }
           }
+          if (++pend == 3) {
+            flush();
+            pend = 0;
+          }
         }
+        flush();
       }
       uint16_t* hrow = hist16 + lane * LS;
 #pragma unroll
@@ -446,7 +466,7 @@ __global__ void __launch_bounds__(32 * kHistWarps, 3) tri_hist_kernel(TriHistArg
         if (c < C) {
 #pragma unroll
           for (int d = 0; d < 8; ++d)  // static indices keep H in registers
-            if (d < k) hrow[c * k + d] = static_cast<uint16_t>(H[c][d >> 2] >> (16 * (d & 3)));
+            if (d < k) hrow[c * k + d] = static_cast<uint16_t>(H[c][d >> 1] >> (16 * (d & 1)));
         }
       }
       __syncwarp();
@@ -474,6 +494,7 @@ __global__ void __launch_bounds__(32 * kHistWarps, 3) tri_hist_kernel(TriHistArg
       __syncwarp();
     }
     if (live) {
+      uint32_t updl = 0;  // 32-bit per-edge term counter, folded into upd below
       const uint32_t a = A.out_src[j], b = A.out_nbr[j];
       const uint32_t sab = A.out_slot[j], sba = A.rev[sab];
       const uint64_t cas = load_colors(A.chi, a), cbs = load_colors(A.chi, b);
@@ -513,18 +534,19 @@ __global__ void __launch_bounds__(32 * kHistWarps, 3) tri_hist_kernel(TriHistArg
           for (uint32_t i = 0; i < A.P2; ++i) {
             const uint32_t* tt = terms + static_cast<size_t>(tb + i) * A.nterm;
             uint64_t v = 0;
+            // branch-free multiply-add: lanes of a warp hold different
+            // colour pairs, so per-term zero tests would only diverge
+#pragma unroll 4
             for (int t = 0; t < A.nterm; ++t) {
               const uint32_t x = tt[t];
-              if (x == ~0u) continue;
-              const uint32_t hc = hval(x >> 16);
-              if (!hc) continue;
-              const uint64_t f = Fs ? Fs[x & 0xFFFFu] : 1ull;
-              if (!f) continue;
+              const bool ok = x != ~0u;
+              const uint32_t hc = ok ? hval(x >> 16) : 0u;
+              const uint64_t f = Fs ? (ok ? Fs[x & 0xFFFFu] : 0ull) : 1ull;
               ovf |= __umul64hi(f, hc) != 0;
               const uint64_t fh = f * hc;
               v += fh;
               ovf |= v < fh;
-              ++upd;
+              updl += fh != 0;
             }
             if (A.out_kind == 2) {
               A.out[orow + i] = v;
@@ -553,18 +575,17 @@ __global__ void __launch_bounds__(32 * kHistWarps, 3) tri_hist_kernel(TriHistArg
             for (uint32_t i = 0; i < A.P2p; ++i) {
               const uint32_t* tt = termsp + static_cast<size_t>(tb + i) * A.ntermp;
               uint64_t v = 0;
+#pragma unroll 4
               for (int t = 0; t < A.ntermp; ++t) {
                 const uint32_t x = tt[t];
-                if (x == ~0u) continue;
-                const uint32_t hc = hval(x >> 16);
-                if (!hc) continue;
-                const uint64_t f = T[x & 0xFFFFu];
-                if (!f) continue;
+                const bool ok = x != ~0u;
+                const uint32_t hc = ok ? hval(x >> 16) : 0u;
+                const uint64_t f = ok ? T[x & 0xFFFFu] : 0ull;
                 ovf |= __umul64hi(f, hc) != 0;
                 const uint64_t fh = f * hc;
                 v += fh;
                 ovf |= v < fh;
-                ++upd;
+                updl += fh != 0;
               }
               if (A.pout_kind == 2) {
                 A.pout[static_cast<uint64_t>(o ? sba : sab) * A.rsop + c * A.Poutp + i] = v;
@@ -592,6 +613,7 @@ __global__ void __launch_bounds__(32 * kHistWarps, 3) tri_hist_kernel(TriHistArg
             ovf |= local[cc] < acc;
           }
       }
+      upd += updl;
     }
     __syncwarp();
   }
