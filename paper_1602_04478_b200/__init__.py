@@ -34,7 +34,9 @@ from typing import Iterable, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmotif_b200.so")
+# MB_LIB_PATH: a developer override (an alternative in-tree build of the same
+# library, e.g. a tuning variant from tools/build_variant.sh)
+LIB_PATH = os.environ.get("MB_LIB_PATH") or os.path.join(_HERE, "libmotif_b200.so")
 
 __all__ = [
     "MotifError", "ParseError", "TreewidthError", "CountOverflowError", "BudgetError",
