@@ -136,7 +136,7 @@ class Reference:
             "ref_plan_canonical": [P, C.c_int, C.c_char_p, C.c_int],
             "ref_count_colorful": [P, u8p, C.c_int, P, C.c_int, C.c_int, C.c_int, u64p],
             "ref_count_ops": [P, u8p, C.c_int, P, C.c_int, u64p, u64p],
-            "ref_count_batch": [P, u8p, C.c_int, C.c_int, P, C.c_int, C.c_int, u64p],
+            "ref_count_batch": [P, u8p, C.c_int, C.c_int, P, C.c_int, C.c_int, C.c_int, u64p],
             "ref_brute_colorful": [P, P, u8p, C.c_int, C.c_uint64, u64p],
             "ref_brute_matches": [P, P, C.c_uint64, u64p],
             "ref_automorphism_count": [P, u64p],
@@ -225,11 +225,13 @@ class Reference:
                                            C.byref(out)))
         return out.value
 
-    def count_batch(self, g, plan, chis, engine=1, threads=1):
+    def count_batch(self, g, plan, chis, engine=1, threads=1, workers=1):
+        """threads colourings at a time; workers > 1 runs each through the
+        reference's BSP executor (parallel_count) on that many OpenMP workers."""
         c = np.ascontiguousarray(chis, dtype=np.uint8)
         out = np.zeros(c.shape[0], dtype=np.uint64)
         self._ck(self.L.ref_count_batch(g.h, _p(c, C.c_uint8), c.shape[0], plan.k, plan.h, engine, threads,
-                                        _p(out, C.c_uint64)))
+                                        workers, _p(out, C.c_uint64)))
         return out
 
     def count_ops(self, g, plan, chi, engine=1):

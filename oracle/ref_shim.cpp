@@ -166,10 +166,11 @@ int ref_count_colorful(void* gp, const uint8_t* chi, int k, void* pp, int tree_i
 }
 
 // count_colorful for `nc` colourings (n bytes each) on up to `threads` host
-// threads, one colouring per thread at a time (the reference's estimate()
+// threads, one colouring per thread at a time (workers > 1: each colouring
+// through parallel_count's BSP executor, runtime.cpp:311) (the reference's estimate()
 // parallelises the same way, estimate.cpp:149).  Returns the first error.
 int ref_count_batch(void* gp, const uint8_t* chis, int nc, int k, void* pp, int engine, int threads,
-                    uint64_t* out) {
+                    int workers, uint64_t* out) {
   auto* rg = static_cast<RefGraph*>(gp);
   auto* p = static_cast<RefPlan*>(pp);
   const uint32_t n = rg->g.num_vertices();
@@ -184,8 +185,11 @@ int ref_count_batch(void* gp, const uint8_t* chis, int nc, int k, void* pp, int 
         motif::Coloring col;
         col.k = k;
         col.chi.assign(chis + static_cast<size_t>(c) * n, chis + static_cast<size_t>(c + 1) * n);
-        out[c] = motif::count_colorful(rg->g, col, rg->ord, p->trees[p->selected],
-                                       engine == 0 ? motif::EngineKind::PS : motif::EngineKind::DB);
+        const auto kind = engine == 0 ? motif::EngineKind::PS : motif::EngineKind::DB;
+        if (workers <= 1)
+          out[c] = motif::count_colorful(rg->g, col, rg->ord, p->trees[p->selected], kind);
+        else  // the reference's BSP executor: one colouring over `workers` OpenMP workers
+          out[c] = motif::parallel_count(rg->g, col, p->trees[p->selected], kind, motif::Partition(n, workers));
       } catch (const std::exception& e) {
         std::lock_guard<std::mutex> lk(mu);
         if (!rc) {

@@ -66,6 +66,8 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
   u64* Zw = Zg + (lane / 32) * gstride;  // this warp's copy
   u64* O = Z + A.C * A.PZ;
   uint64_t upd = 0;
+  const bool cpow2 = (A.C & (A.C - 1)) == 0;  // full batches: C = 8
+  const int clog = __ffs(A.C) - 1;
   for (uint32_t gi = blockIdx.x * kGroups + g; gi < nv; gi += gridDim.x * kGroups) {
     const uint32_t x = vlist[gi];
     for (uint32_t i = lane; i < gstride * kWarpsPerGroup; i += GROUP) Zg[i] = 0;
@@ -77,7 +79,7 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
     // warp, and a neighbour's C rows are read as one contiguous span
     const uint32_t items = deg * static_cast<uint32_t>(A.C);
     for (uint32_t it = lane; it < items; it += GROUP) {
-      const uint32_t j = it / static_cast<uint32_t>(A.C);
+      const uint32_t j = cpow2 ? it >> clog : it / static_cast<uint32_t>(A.C);
       const int c = static_cast<int>(it - j * static_cast<uint32_t>(A.C));
       const uint32_t y = __ldg(A.adj + base + j);
       const uint32_t cx = color_of(cxs, c), cy = A.chi[static_cast<uint64_t>(y) * kChiStride + c];
@@ -93,13 +95,19 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
       }
       if (cy == cx) continue;
       const uint64_t* row = A.ub + static_cast<uint64_t>(y) * A.rsb + c * pb;
-      for (uint32_t ib = 0; ib < pb; ++ib) {
-        const uint64_t v = __ldg(row + ib);
-        if (!v) continue;
-        const uint16_t t = my[ib];
-        if (t == 0xFFFF) continue;
-        atomic_add_ck(Zc + t, v, A.err);
-        ++upd;
+      for (uint32_t i0 = 0; i0 < pb; i0 += 8) {
+        // the row's loads are issued together, then consumed
+        uint64_t r[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) r[u] = i0 + u < pb ? __ldg(row + i0 + u) : 0ull;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (!r[u]) continue;
+          const uint16_t t = my[i0 + u];
+          if (t == 0xFFFF) continue;
+          atomic_add_ck(Zc + t, r[u], A.err);
+          ++upd;
+        }
       }
     }
     if (GROUP == 32) {
