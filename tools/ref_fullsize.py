@@ -12,7 +12,8 @@ rg = R.graph(g.num_vertices(), g.edges())
 rp = R.plan(6, [(0,1),(1,2),(2,0),(1,3),(3,2),(2,4),(4,5)])
 chis = np.stack([mb.random_coloring(g, 6, s) for s in range(100, 100 + nc)])
 ncpu = len(os.sched_getaffinity(0))
-threads, workers = nc, max(1, ncpu // nc)
+threads = nc
+workers = int(sys.argv[2]) if len(sys.argv) > 2 else max(1, ncpu // nc)
 print("cpus", ncpu, "threads", threads, "workers", workers, flush=True)
 t = time.time(); out = R.count_batch(rg, rp, chis, threads=threads, workers=workers); dt = time.time() - t
 print(f"{nc} colourings in {dt:.1f}s -> {nc/dt:.5f} col/s", out.tolist(), flush=True)
