@@ -280,6 +280,7 @@ struct MergeArgs {
   uint64_t* out;
   uint32_t Pout, rso;
   u64* scalar;
+  uint32_t scalar_mult;  // rotation-symmetric root cycle: the h = 0 count times L
   int* err;
   u64* updates;
 };
@@ -364,7 +365,7 @@ __global__ void __launch_bounds__(256) k_half_merge(MergeArgs A) {
   }
   if (A.out_kind == 1) {
     for (int o = 16; o > 0; o >>= 1) local = add_ck(local, __shfl_down_sync(0xffffffffu, local, o), A.err);
-    if ((threadIdx.x & 31) == 0 && local) atomic_add_ck(A.scalar, local, A.err);
+    if ((threadIdx.x & 31) == 0 && local) atomic_add_ck(A.scalar, mul_ck(local, A.scalar_mult, A.err), A.err);
   }
   for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(0xffffffffu, upd, o);
   if ((threadIdx.x & 31) == 0 && upd) atomicAdd(A.updates, static_cast<u64>(upd));
@@ -433,6 +434,9 @@ __global__ void k_gather_rows(const uint64_t* __restrict__ idx, const uint64_t* 
 struct PairBuild {  // merge contributions of a pair-keyed block
   std::vector<DBuf> keys, rows;
   std::vector<uint64_t> counts;
+  uint64_t pending = 0;  // contributions not yet folded into the running table
+  DBuf run_key, run_pay;  // running aggregate (sorted distinct keys)
+  uint64_t run_n = 0;
 };
 
 struct CycleRunner {
@@ -448,6 +452,7 @@ struct CycleRunner {
   DBuf sort_tmp;
   uint64_t mem_budget = 6ull << 30;  // bytes of per-hop scratch per batch
   bool force = false;                 // single-anchor batch: no further split
+  uint32_t h_mult = 1;                // Eq. 1 terms represented by each evaluated h
   PairBuild pairs;
 
   static uint64_t binom(int a, int b) { return binom_host(a, b); }
@@ -653,6 +658,7 @@ struct CycleRunner {
     M.key_src0 = ks0, M.key_src1 = ks1;
     M.out = C.out.data, M.Pout = C.out.P, M.rso = C.out.rs;
     M.scalar = scalar, M.err = err, M.updates = upd;
+    M.scalar_mult = h_mult;
     DBuf ck, cr;
     if (M.out_kind == 4) {
       ck.alloc(A.n * 8);
@@ -664,13 +670,60 @@ struct CycleRunner {
       pairs.keys.push_back(std::move(ck));
       pairs.rows.push_back(std::move(cr));
       pairs.counts.push_back(A.n);
+      pairs.pending += A.n;
+      // many anchors contribute to the same boundary pair (theta, n = 2000:
+      // 162 M contributions, 2.5 M pairs): fold them in before they pile up
+      if (pairs.pending * (C.out.P + 1) * 8ull > mem_budget / 2) compact_pairs(C.out.P);
     }
+    return true;
+  }
+
+  // Folds the pending contributions into the running pair table.
+  void compact_pairs(uint32_t P) {
+    if (pairs.pending == 0) return;
+    const uint64_t W = pairs.pending + pairs.run_n;
+    DBuf allk(W * 8), allr(std::max<uint64_t>(W * P, 1) * 8);
+    uint64_t o = 0;
+    auto put = [&](const DBuf& k, const DBuf& r, uint64_t c) {
+      if (!c) return;
+      MB_CUDA(cudaMemcpyAsync(allk.as<uint64_t>() + o, k.p, c * 8, cudaMemcpyDeviceToDevice, stream));
+      MB_CUDA(cudaMemcpyAsync(allr.as<uint64_t>() + o * P, r.p, c * P * 8, cudaMemcpyDeviceToDevice, stream));
+      o += c;
+    };
+    put(pairs.run_key, pairs.run_pay, pairs.run_n);
+    for (size_t i = 0; i < pairs.counts.size(); ++i) put(pairs.keys[i], pairs.rows[i], pairs.counts[i]);
+    pairs.keys.clear();
+    pairs.rows.clear();
+    pairs.counts.clear();
+    pairs.run_key.release();
+    pairs.run_pay.release();
+    static const bool dbg = std::getenv("MB_DEBUG_HOPS") != nullptr;
+    uint64_t nk = 0;
+    aggregate(allk, allr, W, P, pairs.run_key, pairs.run_pay, nk);
+    if (dbg) fprintf(stderr, "pairs: %llu pending + %llu running -> %llu\n", (unsigned long long)pairs.pending,
+                     (unsigned long long)pairs.run_n, (unsigned long long)nk);
+    pairs.run_n = nk;
+    pairs.pending = 0;
+  }
+
+  // A root cycle with no boundary and no annotation on any node or edge: every
+  // rotation maps the labelled matches whose highest vertex sits at position h
+  // one-to-one onto those with it at h + 1, so all L terms of Eq. 1 are equal
+  // and the h = 0 term times L is exact (configs 0 and 2).
+  static bool rotation_symmetric(const CycleDesc& C) {
+    if (!C.bpos.empty() || C.out.kind != 1) return false;
+    for (int q = 0; q < C.L; ++q)
+      if (C.node[q].kind || C.edge[q].kind) return false;
     return true;
   }
 
   void solve(const CycleDesc& C) {
     const uint32_t first_batch = std::max<uint32_t>(1, std::min<uint32_t>(G.n, 1u << 20));
-    for (int h = 0; h < C.L; ++h) {
+    static const bool no_sym = std::getenv("MB_NO_CYCLE_SYMMETRY") != nullptr;
+    const bool sym = rotation_symmetric(C) && !no_sym;
+    h_mult = sym ? static_cast<uint32_t>(C.L) : 1u;
+    const int nh = sym ? 1 : C.L;
+    for (int h = 0; h < nh; ++h) {
       std::vector<std::pair<uint32_t, uint32_t>> todo;
       for (uint32_t x = 0; x < G.n; x += first_batch) todo.push_back({x, std::min(first_batch, G.n - x)});
       std::reverse(todo.begin(), todo.end());
@@ -690,25 +743,16 @@ struct CycleRunner {
   // sorted pair table with CSR rows (and the transposed copy).
   void finish_pairs(uint32_t P, DBuf& key, DBuf& pay, uint64_t& nk, DBuf& off, DBuf& cols, DBuf& off_t,
                     DBuf& cols_t, DBuf& pay_t) {
-    uint64_t W = 0;
-    for (uint64_t c : pairs.counts) W += c;
-    nk = 0;
-    if (W) {
-      DBuf allk(W * 8), allr(W * P * 8);
-      uint64_t o = 0;
-      for (size_t i = 0; i < pairs.counts.size(); ++i) {
-        const uint64_t c = pairs.counts[i];
-        MB_CUDA(cudaMemcpyAsync(allk.as<uint64_t>() + o, pairs.keys[i].p, c * 8, cudaMemcpyDeviceToDevice, stream));
-        MB_CUDA(cudaMemcpyAsync(allr.as<uint64_t>() + o * P, pairs.rows[i].p, c * P * 8, cudaMemcpyDeviceToDevice,
-                                stream));
-        o += c;
-      }
-      pairs = PairBuild{};
-      aggregate(allk, allr, W, P, key, pay, nk);
+    compact_pairs(P);
+    nk = pairs.run_n;
+    if (nk) {
+      key = std::move(pairs.run_key);
+      pay = std::move(pairs.run_pay);
     } else {
       key.alloc(8);
       pay.alloc(8);
     }
+    pairs = PairBuild{};
     build_csr(key, nk, off, cols);
     // transpose: swap the two keys, sort, gather rows
     DBuf tk(std::max<uint64_t>(nk, 1) * 8), idx(std::max<uint64_t>(nk, 1) * 8), sk(std::max<uint64_t>(nk, 1) * 8),

@@ -31,28 +31,54 @@ namespace mb {
 
 using u64 = unsigned long long;
 
+// Device buffers are stream-ordered (cudaMallocAsync / cudaFreeAsync from the
+// device's pool, which keeps freed blocks): the cycle engine allocates scratch
+// per hop, and a plain cudaFree would synchronise the device every time.  A
+// buffer is allocated on the calling thread's current engine stream
+// (StreamScope) and freed on the stream it was allocated on.  `persistent`
+// buffers (process-lifetime LUTs) use cudaMalloc.
+thread_local cudaStream_t t_dbuf_stream = nullptr;
+
+struct StreamScope {  // sets the allocation stream for the engine entry point's duration
+  cudaStream_t prev;
+  explicit StreamScope(cudaStream_t s) : prev(t_dbuf_stream) { t_dbuf_stream = s; }
+  ~StreamScope() { t_dbuf_stream = prev; }
+};
+
 struct DBuf {
   void* p = nullptr;
   size_t bytes = 0;
+  cudaStream_t s = nullptr;
+  bool persistent = false;
   DBuf() = default;
   explicit DBuf(size_t b) { alloc(b); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr, o.bytes = 0; }
+  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes), s(o.s), persistent(o.persistent) { o.p = nullptr, o.bytes = 0; }
   DBuf& operator=(DBuf&& o) noexcept {
     release();
-    p = o.p, bytes = o.bytes;
+    p = o.p, bytes = o.bytes, s = o.s, persistent = o.persistent;
     o.p = nullptr, o.bytes = 0;
     return *this;
   }
   ~DBuf() { release(); }
   void alloc(size_t b) {
     release();
-    if (b) MB_CUDA(cudaMalloc(&p, b));
+    if (b) {
+      if (persistent) {
+        MB_CUDA(cudaMalloc(&p, b));
+      } else {
+        s = t_dbuf_stream;
+        MB_CUDA(cudaMallocAsync(&p, b, s));
+      }
+    }
     bytes = b;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      if (persistent) cudaFree(p);
+      else cudaFreeAsync(p, s);
+    }
     p = nullptr;
     bytes = 0;
   }
@@ -94,6 +120,7 @@ struct LutHolder {
     L.off[kMaxColors + 1] = static_cast<uint32_t>(masks.size());
     for (int c = 0; c <= kMaxColors; ++c)
       for (int i = 0; i <= kMaxColors + 1; ++i) L.binom[c][i] = static_cast<uint32_t>(binom_host(c, i));
+    unrank.persistent = true;
     unrank.alloc(masks.size() * sizeof(uint16_t));
     MB_CUDA(cudaMemcpy(unrank.p, masks.data(), masks.size() * sizeof(uint16_t),
                        cudaMemcpyHostToDevice));
