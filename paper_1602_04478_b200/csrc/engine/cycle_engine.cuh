@@ -44,6 +44,7 @@ struct GraphView {
   const uint32_t* rev;
   const uint32_t* rank;
   const uint8_t* chi;  // pre-offset to the colouring; stride kChiStride
+  int ordered;         // device ids descend with rank: rank(w) < rank(x) <=> w > x
 };
 
 __device__ __forceinline__ uint32_t vcol(const GraphView& G, uint32_t v) {
@@ -61,7 +62,8 @@ struct HopArgs {
   int first_hop;  // input keys are (x, x): fixed colours {chi x}
   int in_has_r;
   // work decomposition
-  const uint64_t* woff;  // exclusive scan of per-entry degree (n_in + 1)
+  const uint64_t* woff;  // exclusive scan of per-entry work (n_in + 1)
+  const uint64_t* sstart;  // per entry: first relation slot walked
   uint64_t W;
   // hop relation: rows roff/radj (graph CSR or a pair table's CSR)
   const uint64_t* roff;
@@ -104,27 +106,74 @@ __device__ __forceinline__ void unpack_key(uint64_t key, int has_r, int bits, ui
   x = static_cast<uint32_t>(key >> bits);
 }
 
+// Per frontier entry (x, v): the relation row of v, restricted to neighbours
+// ranked below the anchor x.  With degree-ordered device ids those are exactly
+// the ids above x, i.e. a suffix of the sorted row (graph CSR and pair-table
+// CSR rows are both sorted), so the work is counted and walked without the
+// neighbours that would only be discarded.
 __global__ void k_hop_work(const uint64_t* __restrict__ key_in, uint64_t n_in, int has_r, int bits,
-                           const uint64_t* __restrict__ off, uint64_t* __restrict__ work) {  // off: relation rows
+                           const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj, int ordered,
+                           uint64_t* __restrict__ work, uint64_t* __restrict__ sstart) {
   const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (i >= n_in) return;
   uint32_t x, v, r;
   unpack_key(key_in[i], has_r, bits, x, v, r);
-  work[i] = off[v + 1] - off[v];
+  uint64_t lo = off[v], hi = off[v + 1];
+  if (ordered) {
+    uint64_t a = lo, b = hi;  // first slot with adj > x
+    while (a < b) {
+      const uint64_t mid = (a + b) >> 1;
+      if (adj[mid] <= x) a = mid + 1; else b = mid;
+    }
+    lo = a;
+  }
+  sstart[i] = lo;
+  work[i] = hi - lo;
 }
 
+constexpr int kHopTile = 256;  // items per CTA of k_hop_expand
+
 // One thread per (frontier entry, neighbour) work item; writes the item's key
-// (UINT64_MAX when it contributes nothing) and its dense colour-set row.
-__global__ void __launch_bounds__(256) k_hop_expand(HopArgs A) {
-  const uint64_t item = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (item >= A.W) return;
-  // entry = last i with woff[i] <= item
-  uint64_t lo = 0, hi = A.n_in;
-  while (hi - lo > 1) {
-    const uint64_t mid = (lo + hi) >> 1;
-    if (A.woff[mid] <= item) lo = mid; else hi = mid;
+// (UINT64_MAX when it contributes nothing) and its dense colour-set row.  The
+// CTA locates its items' entries once: the woff span of its tile is staged in
+// shared memory and each thread searches there.
+__global__ void __launch_bounds__(kHopTile) k_hop_expand(HopArgs A) {
+  __shared__ uint64_t s_woff[kHopTile + 1];
+  __shared__ uint64_t s_e0, s_cnt;
+  const uint64_t item0 = static_cast<uint64_t>(blockIdx.x) * kHopTile;
+  const uint64_t item = item0 + threadIdx.x;
+  auto entry_of = [&](uint64_t it) {  // last i with woff[i] <= it
+    uint64_t lo = 0, hi = A.n_in;
+    while (hi - lo > 1) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (A.woff[mid] <= it) lo = mid; else hi = mid;
+    }
+    return lo;
+  };
+  if (threadIdx.x == 0) {
+    const uint64_t e0 = entry_of(item0);
+    const uint64_t e1 = entry_of(min(item0 + kHopTile - 1, A.W - 1));
+    s_e0 = e0;
+    s_cnt = e1 - e0 + 1;
   }
-  const uint64_t i = lo;
+  __syncthreads();
+  const uint64_t e0 = s_e0, cnt = s_cnt;
+  const bool staged = cnt <= kHopTile;
+  if (staged)
+    for (uint64_t j = threadIdx.x; j <= cnt && e0 + j <= A.n_in; j += kHopTile) s_woff[j] = A.woff[e0 + j];
+  __syncthreads();
+  if (item >= A.W) return;
+  uint64_t i;
+  if (staged) {
+    uint64_t lo = 0, hi = cnt;
+    while (hi - lo > 1) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (s_woff[mid] <= item) lo = mid; else hi = mid;
+    }
+    i = e0 + lo;
+  } else {
+    i = entry_of(item);
+  }
   uint32_t x, v, r;
   unpack_key(A.key_in[i], A.in_has_r, A.bits, x, v, r);
   if (x >= A.G.n || v >= A.G.n) {
@@ -132,7 +181,7 @@ __global__ void __launch_bounds__(256) k_hop_expand(HopArgs A) {
     A.key_out[item] = ~0ull;
     return;
   }
-  const uint64_t slot = A.roff[v] + (item - A.woff[i]);
+  const uint64_t slot = A.sstart[i] + (item - A.woff[i]);
   if (slot >= A.roff[A.G.n]) {
     atomicOr(A.err, 64);
     A.key_out[item] = ~0ull;
@@ -148,7 +197,7 @@ __global__ void __launch_bounds__(256) k_hop_expand(HopArgs A) {
   for (uint32_t j = 0; j < A.P_out; ++j) row[j] = 0;
   uint64_t key = ~0ull;
   bool any = false;
-  if (A.G.rank[w] < A.G.rank[x]) {
+  if (A.G.ordered || A.G.rank[w] < A.G.rank[x]) {
     const uint32_t cx = vcol(A.G, x), cv = vcol(A.G, v), cw = vcol(A.G, w);
     const uint32_t fin = A.first_hop ? (1u << cx) : ((1u << cx) | (1u << cv));
     const uint32_t fout = (1u << cx) | (1u << cw);
@@ -215,12 +264,16 @@ __global__ void __launch_bounds__(256) k_hop_expand(HopArgs A) {
     }
   }
   A.key_out[item] = key;
-  if (any) atomicAdd(A.updates, 1ull);
+  const unsigned am = __activemask();
+  const unsigned bal = __ballot_sync(am, any);
+  if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(am) - 1) && bal)
+    atomicAdd(A.updates, static_cast<u64>(__popc(bal)));
 }
 
-__global__ void k_iota(uint64_t* __restrict__ out, uint64_t W) {
+template <class T>
+__global__ void k_iota(T* __restrict__ out, uint64_t W) {
   const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (i < W) out[i] = i;
+  if (i < W) out[i] = static_cast<T>(i);
 }
 
 __global__ void k_seg_heads(const uint64_t* __restrict__ keys, uint64_t W, uint64_t* __restrict__ head) {
@@ -230,7 +283,7 @@ __global__ void k_seg_heads(const uint64_t* __restrict__ keys, uint64_t W, uint6
 }
 
 // seg = inclusive-scan(head) - 1; accumulate the item's row into its segment.
-__global__ void k_seg_accumulate(const uint64_t* __restrict__ keys, const uint64_t* __restrict__ idx,
+__global__ void k_seg_accumulate(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ idx,
                                  const uint64_t* __restrict__ segx, const uint64_t* __restrict__ head,
                                  const uint64_t* __restrict__ rows, uint32_t P, uint64_t W,
                                  uint64_t* __restrict__ key_out, uint64_t* __restrict__ pay_out, int* err) {
@@ -238,7 +291,7 @@ __global__ void k_seg_accumulate(const uint64_t* __restrict__ keys, const uint64
   if (i >= W || keys[i] == ~0ull) return;
   const uint64_t seg = segx[i] + head[i] - 1;  // exclusive scan + own head = inclusive
   if (head[i]) key_out[seg] = keys[i];
-  const uint64_t* row = rows + idx[i] * P;
+  const uint64_t* row = rows + static_cast<uint64_t>(idx[i]) * P;
   for (uint32_t j = 0; j < P; ++j)
     if (row[j]) atomic_add_ck(reinterpret_cast<u64*>(pay_out + seg * P + j), row[j], err);
 }
@@ -457,31 +510,42 @@ struct CycleRunner {
 
   static uint64_t binom(int a, int b) { return binom_host(a, b); }
 
+  double wait_s = 0;  // host time blocked in d2h (MB_DEBUG_BATCH)
+
   uint64_t d2h(const uint64_t* p) {
     uint64_t v = 0;
+    const auto t0 = std::chrono::steady_clock::now();
     MB_CUDA(cudaMemcpyAsync(&v, p, 8, cudaMemcpyDeviceToHost, stream));
     MB_CUDA(cudaStreamSynchronize(stream));
+    wait_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     return v;
   }
 
-  void sort_pairs(const uint64_t* kin, uint64_t* kout, const uint64_t* vin, uint64_t* vout, uint64_t W) {
+  // Radix sort of (key, value) pairs on the low `end_bit` key bits only:
+  // packed keys use 2 or 3 fields of `bits` bits, so most of the 64 are zero.
+  template <class V>
+  void sort_pairs(const uint64_t* kin, uint64_t* kout, const V* vin, V* vout, uint64_t W, int end_bit) {
+    end_bit = std::min(64, std::max(1, end_bit));
     size_t tmp = 0;
-    MB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, static_cast<int64_t>(W), 0, 64, stream));
+    MB_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, static_cast<int64_t>(W), 0, end_bit,
+                                            stream));
     if (sort_tmp.bytes < tmp) sort_tmp.alloc(tmp);
     launch("cub_radix_sort", [&] {
-      MB_CUDA(cub::DeviceRadixSort::SortPairs(sort_tmp.p, tmp, kin, kout, vin, vout, static_cast<int64_t>(W), 0, 64,
-                                              stream));
+      MB_CUDA(cub::DeviceRadixSort::SortPairs(sort_tmp.p, tmp, kin, kout, vin, vout, static_cast<int64_t>(W), 0,
+                                              end_bit, stream));
     });
   }
 
   // Sort contributions (keys[W], rows[W][P]) and add equal keys: the
   // reference's hash-map accumulate (table.cpp:190) as sort + segmented add.
-  // Keys equal to UINT64_MAX are dropped.
+  // Keys equal to UINT64_MAX are dropped.  Valid keys are below 2^key_bits;
+  // sorting key_bits + 1 bits keeps the sentinel (that bit set) after them.
   void aggregate(const DBuf& keys, const DBuf& rows, uint64_t W, uint32_t P, DBuf& out_key, DBuf& out_pay,
-                 uint64_t& out_n) {
-    DBuf idx(W * 8), skeys(W * 8), sidx(W * 8);
-    launch("cycle_iota", [&] { k_iota<<<grid_for(W, 256), 256, 0, stream>>>(idx.as<uint64_t>(), W); });
-    sort_pairs(keys.as<uint64_t>(), skeys.as<uint64_t>(), idx.as<uint64_t>(), sidx.as<uint64_t>(), W);
+                 uint64_t& out_n, int key_bits) {
+    if (W >= 0xFFFFFFFFull) fail(kSpec, "cycle engine: more than 2^32 contributions in one aggregation");
+    DBuf idx(W * 4), skeys(W * 8), sidx(W * 4);
+    launch("cycle_iota", [&] { k_iota<uint32_t><<<grid_for(W, 256), 256, 0, stream>>>(idx.as<uint32_t>(), W); });
+    sort_pairs(keys.as<uint64_t>(), skeys.as<uint64_t>(), idx.as<uint32_t>(), sidx.as<uint32_t>(), W, key_bits + 1);
     DBuf head((W + 1) * 8), segx((W + 1) * 8);
     MB_CUDA(cudaMemsetAsync(head.p, 0, (W + 1) * 8, stream));
     launch("cycle_seg_heads", [&] {
@@ -494,7 +558,7 @@ struct CycleRunner {
     MB_CUDA(cudaMemsetAsync(out_pay.p, 0, out_pay.bytes, stream));
     if (out_n)
       launch("cycle_seg_accumulate", [&] {
-        k_seg_accumulate<<<grid_for(W, 256), 256, 0, stream>>>(skeys.as<uint64_t>(), sidx.as<uint64_t>(),
+        k_seg_accumulate<<<grid_for(W, 256), 256, 0, stream>>>(skeys.as<uint64_t>(), sidx.as<uint32_t>(),
                                                                segx.as<uint64_t>(), head.as<uint64_t>(),
                                                                rows.as<uint64_t>(), P, W, out_key.as<uint64_t>(),
                                                                out_pay.as<uint64_t>(), err);
@@ -502,22 +566,29 @@ struct CycleRunner {
   }
 
   // Returns false when the hop exceeded the scratch budget (caller splits the batch).
-  bool hop(const Frontier& in, Frontier& out, const Relation& rel, const TabView& nt, bool record, bool first) {
+  uint64_t last_over = 0;  // scratch bytes the last refused hop needed
+
+  bool hop(const Frontier& in, Frontier& out, const Relation& rel, const TabView& nt, bool record, bool first,
+           bool force_hop) {
     out.has_r = in.has_r || record;
     out.s = in.s + 1 + (rel.pay ? rel.s - 2 : 0) + (nt.kind ? nt.s - 1 : 0);
     out.P = static_cast<uint32_t>(binom(k - 2, out.s - 2));
     out.n = 0;
     if (in.n == 0) return true;
-    DBuf work((in.n + 1) * 8), woff((in.n + 1) * 8);
+    DBuf work((in.n + 1) * 8), woff((in.n + 1) * 8), sstart(std::max<uint64_t>(in.n, 1) * 8);
     MB_CUDA(cudaMemsetAsync(work.p, 0, (in.n + 1) * 8, stream));
     launch("cycle_hop_work", [&] {
       k_hop_work<<<grid_for(in.n, 256), 256, 0, stream>>>(in.key.as<uint64_t>(), in.n, in.has_r, bits, rel.off,
-                                                          work.as<uint64_t>());
+                                                          rel.adj, G.ordered, work.as<uint64_t>(),
+                                                          sstart.as<uint64_t>());
     });
     scan(work.as<uint64_t>(), woff.as<uint64_t>(), in.n + 1);
     const uint64_t W = d2h(woff.as<uint64_t>() + in.n);
     if (W == 0) return true;
-    if (W * (out.P * 8ull + 72) > mem_budget && !force) return false;
+    if (W * (out.P * 8ull + 72) > mem_budget && !force_hop) {
+      last_over = W * (out.P * 8ull + 72);
+      return false;
+    }
     DBuf keys(W * 8), rows(W * out.P * 8);
     HopArgs A{};
     A.G = G;
@@ -529,6 +600,7 @@ struct CycleRunner {
     A.first_hop = first;
     A.in_has_r = in.has_r;
     A.woff = woff.as<uint64_t>();
+    A.sstart = sstart.as<uint64_t>();
     A.W = W;
     A.roff = rel.off;
     A.radj = rel.adj;
@@ -550,8 +622,8 @@ struct CycleRunner {
               (unsigned long long)in.n, (unsigned long long)W, in.s, in.P, (int)first, in.has_r, out.has_r,
               (int)record, out.s, out.P, (const void*)A.etab, A.Pe, A.se, A.rse, A.e_rev,
               (unsigned long long)A.n_etab, (const void*)A.ntab, A.Pn, A.sn, A.rsn, bits);
-    launch("cycle_hop_expand", [&] { k_hop_expand<<<grid_for(W, 256), 256, 0, stream>>>(A); });
-    aggregate(keys, rows, W, out.P, out.key, out.pay, out.n);
+    launch("cycle_hop_expand", [&] { k_hop_expand<<<grid_for(W, kHopTile), kHopTile, 0, stream>>>(A); });
+    aggregate(keys, rows, W, out.P, out.key, out.pay, out.n, (out.has_r ? 3 : 2) * bits);
     return true;
   }
 
@@ -574,10 +646,64 @@ struct CycleRunner {
     return r;
   }
 
-  // Builds one half path from h towards d for anchors [x0, x0 + nx).
-  bool half(const CycleDesc& C, int h, int d, bool cw, bool start_ann, bool end_ann, int rec_pos, uint32_t x0,
-            uint32_t nx, Frontier& f) {
+  using Sink = std::function<void(Frontier&)>;
+
+  // Copies entries [i0, i0 + cnt) of a frontier (the slice stays sorted).
+  void slice(const Frontier& f, uint64_t i0, uint64_t cnt, Frontier& a) {
+    a.s = f.s, a.P = f.P, a.has_r = f.has_r, a.n = cnt;
+    a.key.alloc(std::max<uint64_t>(cnt, 1) * 8), a.pay.alloc(std::max<uint64_t>(cnt * f.P, 1) * 8);
+    MB_CUDA(cudaMemcpyAsync(a.key.p, f.key.as<uint64_t>() + i0, cnt * 8, cudaMemcpyDeviceToDevice, stream));
+    MB_CUDA(cudaMemcpyAsync(a.pay.p, f.pay.as<uint64_t>() + i0 * f.P, cnt * f.P * 8, cudaMemcpyDeviceToDevice,
+                            stream));
+  }
+
+  // Walks a half path from position p (frontier cur) to d and hands every
+  // finished frontier part to `sink`.  Over the scratch budget, a
+  // multi-anchor batch returns false (the caller halves the anchor range; no
+  // part has reached the sink then, since parts only arise below).  A
+  // single-anchor batch instead splits the frontier into parts that continue
+  // separately: hops and the final merge are linear in the frontier, so the
+  // parts' contributions add up to the whole (hub anchors of the theta query
+  // reach ~10^8 (v, r) keys in one hop).
+  bool walk(const CycleDesc& C, Frontier& cur, int p, int d, bool cw, bool end_ann, int rec_pos, bool first,
+            const Sink& sink) {
     const int L = C.L;
+    const TabView none{};
+    while (p != d) {
+      const int q = cw ? (p + 1) % L : (p + L - 1) % L;
+      const int e = cw ? p : q;  // cycle edge joining p and q
+      // child keyed (nodes[e], nodes[e+1]) when edge_fwd; we walk p -> q
+      const bool stored_pq = cw ? static_cast<bool>(C.edge_fwd[e]) : !C.edge_fwd[e];
+      const Relation rel = relation(C, e, C.edge[e].kind ? stored_pq : true);
+      const TabView& nt = (q != d || end_ann) ? C.node[q] : none;
+      Frontier nxt;
+      if (!hop(cur, nxt, rel, nt.kind ? nt : none, q == rec_pos, first, false)) {
+        if (!force) return false;
+        if (cur.n > 1) {
+          // as many parts as the refused hop needs budgets (plus slack)
+          const uint64_t parts = std::min<uint64_t>(cur.n, last_over / mem_budget + 2);
+          const uint64_t per = (cur.n + parts - 1) / parts;
+          Frontier whole = std::move(cur);
+          for (uint64_t i0 = 0; i0 < whole.n; i0 += per) {
+            Frontier a;
+            slice(whole, i0, std::min(per, whole.n - i0), a);
+            if (!walk(C, a, p, d, cw, end_ann, rec_pos, first, sink)) return false;
+          }
+          return true;
+        }
+        hop(cur, nxt, rel, nt.kind ? nt : none, q == rec_pos, first, true);  // one entry: no smaller unit
+      }
+      cur = std::move(nxt);
+      first = false;
+      p = q;
+    }
+    sink(cur);
+    return true;
+  }
+
+  // Builds the half path from h towards d for anchors [x0, x0 + nx).
+  bool half(const CycleDesc& C, int h, int d, bool cw, bool start_ann, bool end_ann, int rec_pos, uint32_t x0,
+            uint32_t nx, const Sink& sink) {
     Frontier cur;
     const TabView& hn = C.node[h];
     const bool use_start = start_ann && hn.kind;
@@ -592,24 +718,66 @@ struct CycleRunner {
                                                              cur.P, hn.rs, cur.key.as<uint64_t>(),
                                                              cur.pay.as<uint64_t>());
     });
-    int p = h;
-    bool first = true;
-    const TabView none{};
-    while (p != d) {
-      const int q = cw ? (p + 1) % L : (p + L - 1) % L;
-      const int e = cw ? p : q;  // cycle edge joining p and q
-      // child keyed (nodes[e], nodes[e+1]) when edge_fwd; we walk p -> q
-      const bool stored_pq = cw ? static_cast<bool>(C.edge_fwd[e]) : !C.edge_fwd[e];
-      const Relation rel = relation(C, e, C.edge[e].kind ? stored_pq : true);
-      const TabView& nt = (q != d || end_ann) ? C.node[q] : none;
-      Frontier nxt;
-      if (!hop(cur, nxt, rel, nt.kind ? nt : none, q == rec_pos, first)) return false;
-      cur = std::move(nxt);
-      first = false;
-      p = q;
+    return walk(C, cur, h, d, cw, end_ann, rec_pos, true, sink);
+  }
+
+  // Joins half-path parts: side A (iterated, may carry r) with side B (looked up by (x, v)).
+  void merge(const CycleDesc& C, const Frontier& A, const Frontier& B, int ks0, int ks1) {
+    MergeArgs M{};
+    M.G = G;
+    M.keyA = A.key.as<uint64_t>(), M.payA = A.pay.as<uint64_t>(), M.nA = A.n, M.sA = A.s, M.PA = A.P;
+    M.A_has_r = A.has_r;
+    M.keyB = B.key.as<uint64_t>(), M.payB = B.pay.as<uint64_t>(), M.nB = B.n, M.sB = B.s, M.PB = B.P;
+    M.bits = bits;
+    M.out_kind = C.out.kind == 1 ? 1 : (C.out.kind == 2 ? 2 : (C.out.kind == 3 ? 3 : 4));
+    M.key_src0 = ks0, M.key_src1 = ks1;
+    M.out = C.out.data, M.Pout = C.out.P, M.rso = C.out.rs;
+    M.scalar = scalar, M.err = err, M.updates = upd;
+    M.scalar_mult = h_mult;
+    DBuf ck, cr;
+    if (M.out_kind == 4) {
+      ck.alloc(A.n * 8);
+      cr.alloc(std::max<uint64_t>(A.n * C.out.P, 1) * 8);
+      M.ckey = ck.as<uint64_t>(), M.crow = cr.as<uint64_t>();
     }
-    f = std::move(cur);
-    return true;
+    launch("cycle_merge", [&] { k_half_merge<<<grid_for(A.n, 256), 256, 0, stream>>>(M); });
+    if (M.out_kind == 4) {
+      pairs.keys.push_back(std::move(ck));
+      pairs.rows.push_back(std::move(cr));
+      pairs.counts.push_back(A.n);
+      pairs.pending += A.n;
+      // many anchors contribute to the same boundary pair (theta, n = 2000:
+      // 162 M contributions, 2.5 M pairs): fold them in before they pile up
+      if (pairs.pending * (C.out.P + 1) * 8ull > mem_budget / 2) compact_pairs(C.out.P);
+    }
+  }
+
+  // Folds the pending contributions into the running pair table.
+  void compact_pairs(uint32_t P) {
+    if (pairs.pending == 0) return;
+    const uint64_t W = pairs.pending + pairs.run_n;
+    DBuf allk(W * 8), allr(std::max<uint64_t>(W * P, 1) * 8);
+    uint64_t o = 0;
+    auto put = [&](const DBuf& k, const DBuf& r, uint64_t c) {
+      if (!c) return;
+      MB_CUDA(cudaMemcpyAsync(allk.as<uint64_t>() + o, k.p, c * 8, cudaMemcpyDeviceToDevice, stream));
+      MB_CUDA(cudaMemcpyAsync(allr.as<uint64_t>() + o * P, r.p, c * P * 8, cudaMemcpyDeviceToDevice, stream));
+      o += c;
+    };
+    put(pairs.run_key, pairs.run_pay, pairs.run_n);
+    for (size_t i = 0; i < pairs.counts.size(); ++i) put(pairs.keys[i], pairs.rows[i], pairs.counts[i]);
+    pairs.keys.clear();
+    pairs.rows.clear();
+    pairs.counts.clear();
+    pairs.run_key.release();
+    pairs.run_pay.release();
+    static const bool dbg = std::getenv("MB_DEBUG_HOPS") != nullptr;
+    uint64_t nk = 0;
+    aggregate(allk, allr, W, P, pairs.run_key, pairs.run_pay, nk, 2 * bits);
+    if (dbg) fprintf(stderr, "pairs: %llu pending + %llu running -> %llu\n", (unsigned long long)pairs.pending,
+                     (unsigned long long)pairs.run_n, (unsigned long long)nk);
+    pairs.run_n = nk;
+    pairs.pending = 0;
   }
 
   // Evaluates position h of Eq. 1 for anchors [x0, x0+nx); false = split and
@@ -640,70 +808,27 @@ struct CycleRunner {
     bool rec_cw = false;
     for (int p = h; p != d; p = (p + 1) % L)
       if (p == rec) rec_cw = true;
-    Frontier fp, fm;
-    // plus (clockwise): excludes the start annotation, includes the end (d)
-    if (!half(C, h, d, true, false, true, rec_cw ? rec : -1, x0, nx, fp)) return false;
-    // minus (counter-clockwise): includes the start annotation, excludes the end
-    if (!half(C, h, d, false, true, false, (rec >= 0 && !rec_cw) ? rec : -1, x0, nx, fm)) return false;
-    if (fp.n == 0 || fm.n == 0) return true;
-    const Frontier& A = fp.has_r ? fp : fm;
-    const Frontier& B = fp.has_r ? fm : fp;
-    MergeArgs M{};
-    M.G = G;
-    M.keyA = A.key.as<uint64_t>(), M.payA = A.pay.as<uint64_t>(), M.nA = A.n, M.sA = A.s, M.PA = A.P;
-    M.A_has_r = A.has_r;
-    M.keyB = B.key.as<uint64_t>(), M.payB = B.pay.as<uint64_t>(), M.nB = B.n, M.sB = B.s, M.PB = B.P;
-    M.bits = bits;
-    M.out_kind = C.out.kind == 1 ? 1 : (C.out.kind == 2 ? 2 : (C.out.kind == 3 ? 3 : 4));
-    M.key_src0 = ks0, M.key_src1 = ks1;
-    M.out = C.out.data, M.Pout = C.out.P, M.rso = C.out.rs;
-    M.scalar = scalar, M.err = err, M.updates = upd;
-    M.scalar_mult = h_mult;
-    DBuf ck, cr;
-    if (M.out_kind == 4) {
-      ck.alloc(A.n * 8);
-      cr.alloc(std::max<uint64_t>(A.n * C.out.P, 1) * 8);
-      M.ckey = ck.as<uint64_t>(), M.crow = cr.as<uint64_t>();
-    }
-    launch("cycle_merge", [&] { k_half_merge<<<grid_for(A.n, 256), 256, 0, stream>>>(M); });
-    if (M.out_kind == 4) {
-      pairs.keys.push_back(std::move(ck));
-      pairs.rows.push_back(std::move(cr));
-      pairs.counts.push_back(A.n);
-      pairs.pending += A.n;
-      // many anchors contribute to the same boundary pair (theta, n = 2000:
-      // 162 M contributions, 2.5 M pairs): fold them in before they pile up
-      if (pairs.pending * (C.out.P + 1) * 8ull > mem_budget / 2) compact_pairs(C.out.P);
-    }
-    return true;
-  }
-
-  // Folds the pending contributions into the running pair table.
-  void compact_pairs(uint32_t P) {
-    if (pairs.pending == 0) return;
-    const uint64_t W = pairs.pending + pairs.run_n;
-    DBuf allk(W * 8), allr(std::max<uint64_t>(W * P, 1) * 8);
-    uint64_t o = 0;
-    auto put = [&](const DBuf& k, const DBuf& r, uint64_t c) {
-      if (!c) return;
-      MB_CUDA(cudaMemcpyAsync(allk.as<uint64_t>() + o, k.p, c * 8, cudaMemcpyDeviceToDevice, stream));
-      MB_CUDA(cudaMemcpyAsync(allr.as<uint64_t>() + o * P, r.p, c * P * 8, cudaMemcpyDeviceToDevice, stream));
-      o += c;
+    // plus (clockwise) excludes the start annotation and includes the end (d);
+    // minus (counter-clockwise) includes the start and excludes the end.  The
+    // side that records r is iterated (A); the other is looked up (B), so B's
+    // parts are built first and kept, and A's parts are merged as they come.
+    const bool a_is_plus = rec >= 0 && rec_cw;
+    std::vector<Frontier> bparts;
+    const Sink keep = [&](Frontier& f) {
+      if (f.n) bparts.push_back(std::move(f));
     };
-    put(pairs.run_key, pairs.run_pay, pairs.run_n);
-    for (size_t i = 0; i < pairs.counts.size(); ++i) put(pairs.keys[i], pairs.rows[i], pairs.counts[i]);
-    pairs.keys.clear();
-    pairs.rows.clear();
-    pairs.counts.clear();
-    pairs.run_key.release();
-    pairs.run_pay.release();
-    static const bool dbg = std::getenv("MB_DEBUG_HOPS") != nullptr;
-    uint64_t nk = 0;
-    aggregate(allk, allr, W, P, pairs.run_key, pairs.run_pay, nk);
-    if (dbg) fprintf(stderr, "pairs: %llu pending + %llu running -> %llu\n", (unsigned long long)pairs.pending,
-                     (unsigned long long)pairs.run_n, (unsigned long long)nk);
-    pairs.run_n = nk;
-    pairs.pending = 0;
+    if (a_is_plus) {
+      if (!half(C, h, d, false, true, false, -1, x0, nx, keep)) return false;
+    } else {
+      if (!half(C, h, d, true, false, true, -1, x0, nx, keep)) return false;
+    }
+    if (bparts.empty()) return true;
+    const Sink join = [&](Frontier& a) {
+      if (!a.n) return;
+      for (const Frontier& b : bparts) merge(C, a, b, ks0, ks1);
+    };
+    if (a_is_plus) return half(C, h, d, true, false, true, rec, x0, nx, join);
+    return half(C, h, d, false, true, false, rec >= 0 ? rec : -1, x0, nx, join);
   }
 
   // A root cycle with no boundary and no annotation on any node or edge: every
@@ -719,23 +844,60 @@ struct CycleRunner {
 
   void solve(const CycleDesc& C) {
     const uint32_t first_batch = std::max<uint32_t>(1, std::min<uint32_t>(G.n, 1u << 20));
+    {
+      // per-hop scratch: a quarter of what is free (a hop holds ~4x its rows
+      // while it sorts), within [2, 48] GB
+      size_t fr = 0, tot = 0;
+      if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
+        // blocks the pool keeps mapped but does not use are available too
+        int dev = 0;
+        cudaMemPool_t pool;
+        uint64_t reserved = 0, used = 0;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+          cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
+          cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+        }
+        const uint64_t avail = fr + (reserved > used ? reserved - used : 0);
+        mem_budget = std::min<uint64_t>(48ull << 30, std::max<uint64_t>(2ull << 30, avail / 4));
+      }
+      static const char* mb_env = std::getenv("MB_CYCLE_BUDGET_MB");
+      if (mb_env) mem_budget = std::strtoull(mb_env, nullptr, 10) << 20;
+    }
     static const bool no_sym = std::getenv("MB_NO_CYCLE_SYMMETRY") != nullptr;
     const bool sym = rotation_symmetric(C) && !no_sym;
     h_mult = sym ? static_cast<uint32_t>(C.L) : 1u;
     const int nh = sym ? 1 : C.L;
+    // Anchors are swept in device order (hubs first) with an adaptive batch:
+    // halved when a hop would exceed the scratch budget (the attempt is
+    // discarded), doubled after a success, so heavy anchors run in small
+    // batches and the light tail in large ones.
+    static const bool dbg = std::getenv("MB_DEBUG_BATCH") != nullptr;
+    uint64_t ok = 0, failed = 0;
+    const auto t_solve = std::chrono::steady_clock::now();
+    wait_s = 0;
     for (int h = 0; h < nh; ++h) {
-      std::vector<std::pair<uint32_t, uint32_t>> todo;
-      for (uint32_t x = 0; x < G.n; x += first_batch) todo.push_back({x, std::min(first_batch, G.n - x)});
-      std::reverse(todo.begin(), todo.end());
-      while (!todo.empty()) {
-        const auto [x0, nx] = todo.back();
-        todo.pop_back();
+      uint32_t bs = first_batch, cap = first_batch;  // cap: below the last size that failed
+      for (uint32_t x0 = 0; x0 < G.n;) {
+        const uint32_t nx = std::min(bs, G.n - x0);
         force = nx == 1;
-        if (run_batch(C, h, x0, nx)) continue;
-        const uint32_t a = nx / 2;
-        todo.push_back({x0 + a, nx - a});
-        todo.push_back({x0, a});
+        if (run_batch(C, h, x0, nx)) {
+          ++ok;
+          x0 += nx;
+          // anchors get lighter along the sweep: grow, but only slowly past a failure
+          cap = static_cast<uint32_t>(std::min<uint64_t>(first_batch, cap + cap / 4 + 1));
+          bs = static_cast<uint32_t>(std::min<uint64_t>(2ull * nx, cap));
+        } else {
+          ++failed;
+          bs = std::max<uint32_t>(1, nx / 2);
+          cap = bs;
+        }
       }
+    }
+    if (dbg) {
+      MB_CUDA(cudaStreamSynchronize(stream));
+      const double tot = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_solve).count();
+      fprintf(stderr, "cycle L=%d: %llu batches, %llu discarded attempts, budget %.1f GB, %.3f s (%.3f s in d2h)\n",
+              C.L, (unsigned long long)ok, (unsigned long long)failed, mem_budget / 1e9, tot, wait_s);
     }
   }
 
@@ -760,8 +922,8 @@ struct CycleRunner {
     pay_t.alloc(std::max<uint64_t>(nk * P, 1) * 8);
     if (nk) {
       launch("pair_swap", [&] { k_swap_pair_keys<<<grid_for(nk, 256), 256, 0, stream>>>(key.as<uint64_t>(), nk, bits, tk.as<uint64_t>()); });
-      launch("cycle_iota", [&] { k_iota<<<grid_for(nk, 256), 256, 0, stream>>>(idx.as<uint64_t>(), nk); });
-      sort_pairs(tk.as<uint64_t>(), sk.as<uint64_t>(), idx.as<uint64_t>(), sidx.as<uint64_t>(), nk);
+      launch("cycle_iota", [&] { k_iota<uint64_t><<<grid_for(nk, 256), 256, 0, stream>>>(idx.as<uint64_t>(), nk); });
+      sort_pairs(tk.as<uint64_t>(), sk.as<uint64_t>(), idx.as<uint64_t>(), sidx.as<uint64_t>(), nk, 2 * bits);
       launch("pair_gather", [&] {
         k_gather_rows<<<grid_for(nk * P, 256), 256, 0, stream>>>(sidx.as<uint64_t>(), pay.as<uint64_t>(), P, nk,
                                                                  pay_t.as<uint64_t>());
