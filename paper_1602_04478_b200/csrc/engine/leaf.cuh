@@ -26,6 +26,7 @@ struct LeafMapArgs {
   uint32_t Pb, Pa, PZ, Pout;
   uint32_t rsb, rsa, rso;  // row strides (C_alloc * P)
   int sb, sa, sZ, k, C;
+  int unchecked;  // entries provably < 2^62 (host bound): plain adds
   uint64_t* out;
   int* err;
   u64* updates;
@@ -105,7 +106,8 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
           if (!r[u]) continue;
           const uint16_t t = my[i0 + u];
           if (t == 0xFFFF) continue;
-          atomic_add_ck(Zc + t, r[u], A.err);
+          if (A.unchecked) atomicAdd(Zc + t, static_cast<u64>(r[u]));
+          else atomic_add_ck(Zc + t, r[u], A.err);
           ++upd;
         }
       }
@@ -116,7 +118,7 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
       __syncthreads();
       for (uint32_t i = lane; i < A.C * A.PZ; i += GROUP) {
         uint64_t s = Zg[i];
-        for (int w = 1; w < kWarpsPerGroup; ++w) s = add_ck(s, Zg[w * gstride + i], A.err);
+        for (int w = 1; w < kWarpsPerGroup; ++w) s = A.unchecked ? s + Zg[w * gstride + i] : add_ck(s, Zg[w * gstride + i], A.err);
         Z[i] = s;
       }
       __syncthreads();
@@ -138,7 +140,8 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
         const uint32_t Mz = sig_expand(sig_unrank(c_lut, A.sZ - 1, iz), fx);
         const uint32_t Ma = sig_expand(sig_unrank(c_lut, A.sa - 1, ia), fx);
         if ((Mz & Ma) != fx) continue;
-        atomic_add_ck(O + c * A.Pout + sig_index(c_lut, Mz | Ma, fx), mul_ck(z, a, A.err), A.err);
+        if (A.unchecked) atomicAdd(O + c * A.Pout + sig_index(c_lut, Mz | Ma, fx), static_cast<u64>(z * a));
+        else atomic_add_ck(O + c * A.Pout + sig_index(c_lut, Mz | Ma, fx), mul_ck(z, a, A.err), A.err);
         ++upd;
       }
       if (GROUP == 32) __syncwarp(); else __syncthreads();

@@ -382,12 +382,13 @@ __device__ __forceinline__ void build_terms(uint32_t* terms, uint16_t* idx1, int
 #define MB_TRI_MINB 2  // resident CTAs per SM the register budget is sized for (126 regs, no spill;
                        // measured: 3 -> 80 regs + spills, 13.4 ms vs 11.3 ms per 3 batches)
 #endif
+template <bool LANE>
 __global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_hist_kernel(TriHistArgs A) {
   extern __shared__ uint32_t hsm[];
   const int k = A.k, C = A.C;
   const uint32_t PF = A.fkind ? A.PF : 0u;
   const HistSmem L = hist_smem_layout(k, C, A.P2, A.nterm, A.out_kind, A.P2p, A.ntermp, A.pout_kind, PF,
-                                      A.lane_mode);
+                                      LANE);
   uint32_t* terms = hsm;
   uint16_t* idx1 = reinterpret_cast<uint16_t*>(hsm + L.t1);
   uint32_t* termsp = hsm + L.t1 + L.i1;
@@ -406,15 +407,15 @@ __global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_hist_kernel(
 #pragma unroll
   for (int c = 0; c < kChiStride; ++c) local[c] = 0;
   uint64_t upd = 0;
-  const uint32_t LSW = hist_lane_words(C, k, A.lane_mode);
-  const uint32_t LS = A.lane_mode ? 2 * LSW : LSW;  // per-edge row stride in counters
+  const uint32_t LSW = hist_lane_words(C, k, LANE);
+  const uint32_t LS = LANE ? 2 * LSW : LSW;  // per-edge row stride in counters
   const uint64_t nbatch = (A.nitems + 31) / 32;
   for (uint64_t bt = static_cast<uint64_t>(blockIdx.x) * kHistWarps + wid; bt < nbatch;
        bt += static_cast<uint64_t>(gridDim.x) * kHistWarps) {
     const uint64_t j0 = bt * 32;
     const bool live = j0 + lane < A.nitems;
     uint64_t j = j0 + lane;
-    if (A.lane_mode) {
+    if (LANE) {
       // lane owns one oriented edge (edges visited in CN-length order, so the
       // 32 lists of a warp have similar lengths) and counts its common
       // neighbours' colours for all C colourings in registers: 4-bit fields
@@ -501,15 +502,15 @@ __global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_hist_kernel(
       __syncwarp();
     }
     if (live) {
-      uint32_t updl = 0;  // 32-bit per-edge term counter, folded into upd below
+      uint32_t updl = 0;  // nonzero output-entry updates of this edge, folded into upd below
       const uint32_t a = A.out_src[j], b = A.out_nbr[j];
       const uint32_t sab = A.out_slot[j], sba = A.rev[sab];
       const uint64_t cas = load_colors(A.chi, a), cbs = load_colors(A.chi, b);
       for (int c = 0; c < C; ++c) {
         const uint32_t hb = lane * LS + c * k;
-        auto hval = [&](uint32_t d) -> uint32_t { return A.lane_mode ? hist16[hb + d] : hist[hb + d]; };
+        auto hval = [&](uint32_t d) -> uint32_t { return LANE ? hist16[hb + d] : hist[hb + d]; };
         const uint32_t ca = color_of(cas, c), cb = color_of(cbs, c);
-        uint64_t acc = 0;
+        uint64_t acc = 0, tmax = 0;
         for (int o = 0; o < 2; ++o) {
           const uint32_t c0 = o ? cb : ca, c1 = o ? ca : cb;
           const uint64_t orow = static_cast<uint64_t>(o ? sba : sab) * A.rso + c * A.Pout;
@@ -520,6 +521,7 @@ __global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_hist_kernel(
               for (uint32_t i = 0; i < A.P2; ++i) tbuf[o * A.P2 + i] = 0;
             continue;
           }
+          uint64_t fmax = 0;  // OR of the staged factors: decides the unchecked path
           if (PF) {
             // stage this orientation's factor row: independent loads in
             // flight together instead of one dependent gather per term
@@ -533,32 +535,50 @@ __global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_hist_kernel(
               for (int u = 0; u < 8; ++u) r[u] = i0 + u < PF ? __ldg(F + i0 + u) : 0ull;
 #pragma unroll
               for (int u = 0; u < 8; ++u)
-                if (i0 + u < PF) fst[i0 + u] = r[u];
+                if (i0 + u < PF) {
+                  fst[i0 + u] = r[u];
+                  fmax |= r[u];
+                }
             }
           }
           const u64* Fs = PF ? fst : nullptr;
+          // lane-mode counters are < 2^16 and there are <= 15 terms: with every
+          // factor < 2^44 no product or partial sum can reach 2^64
+          const bool safe = LANE && (fmax >> 44) == 0;
           const uint32_t tb = (c0 * k + c1) * A.P2;
           for (uint32_t i = 0; i < A.P2; ++i) {
             const uint32_t* tt = terms + static_cast<size_t>(tb + i) * A.nterm;
             uint64_t v = 0;
             // branch-free multiply-add: lanes of a warp hold different
             // colour pairs, so per-term zero tests would only diverge
+            if (safe) {
 #pragma unroll 4
-            for (int t = 0; t < A.nterm; ++t) {
-              const uint32_t x = tt[t];
-              const bool ok = x != ~0u;
-              const uint32_t hc = ok ? hval(x >> 16) : 0u;
-              const uint64_t f = Fs ? (ok ? Fs[x & 0xFFFFu] : 0ull) : 1ull;
-              ovf |= __umul64hi(f, hc) != 0;
-              const uint64_t fh = f * hc;
-              v += fh;
-              ovf |= v < fh;
-              updl += fh != 0;
+              for (int t = 0; t < A.nterm; ++t) {
+                const uint32_t x = tt[t];
+                const bool ok = x != ~0u;
+                const uint32_t hc = ok ? hval(x >> 16) : 0u;
+                const uint64_t f = Fs ? (ok ? Fs[x & 0xFFFFu] : 0ull) : 1ull;
+                v += f * hc;
+              }
+            } else {
+#pragma unroll 4
+              for (int t = 0; t < A.nterm; ++t) {
+                const uint32_t x = tt[t];
+                const bool ok = x != ~0u;
+                const uint32_t hc = ok ? hval(x >> 16) : 0u;
+                const uint64_t f = Fs ? (ok ? Fs[x & 0xFFFFu] : 0ull) : 1ull;
+                ovf |= __umul64hi(f, hc) != 0;
+                const uint64_t fh = f * hc;
+                v += fh;
+                ovf |= v < fh;
+              }
             }
+            updl += v != 0;
             if (A.out_kind == 2) {
               A.out[orow + i] = v;
             } else if (A.out_kind == 3) {
               tbuf[o * A.P2 + i] = v;
+              tmax |= v;
             } else if (v) {
               if (A.out_kind == 0)
                 {
@@ -579,21 +599,33 @@ __global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_hist_kernel(
             const int osel = ((o == 0) != (A.sw01p != 0)) ? 0 : 1;
             const u64* T = tbuf + osel * A.P2;
             const uint32_t tb = (c0 * k + c1) * A.P2p;
+            const bool safe = LANE && (tmax >> 44) == 0;
             for (uint32_t i = 0; i < A.P2p; ++i) {
               const uint32_t* tt = termsp + static_cast<size_t>(tb + i) * A.ntermp;
               uint64_t v = 0;
+              if (safe) {
 #pragma unroll 4
-              for (int t = 0; t < A.ntermp; ++t) {
-                const uint32_t x = tt[t];
-                const bool ok = x != ~0u;
-                const uint32_t hc = ok ? hval(x >> 16) : 0u;
-                const uint64_t f = ok ? T[x & 0xFFFFu] : 0ull;
-                ovf |= __umul64hi(f, hc) != 0;
-                const uint64_t fh = f * hc;
-                v += fh;
-                ovf |= v < fh;
-                updl += fh != 0;
+                for (int t = 0; t < A.ntermp; ++t) {
+                  const uint32_t x = tt[t];
+                  const bool ok = x != ~0u;
+                  const uint32_t hc = ok ? hval(x >> 16) : 0u;
+                  const uint64_t f = ok ? T[x & 0xFFFFu] : 0ull;
+                  v += f * hc;
+                }
+              } else {
+#pragma unroll 4
+                for (int t = 0; t < A.ntermp; ++t) {
+                  const uint32_t x = tt[t];
+                  const bool ok = x != ~0u;
+                  const uint32_t hc = ok ? hval(x >> 16) : 0u;
+                  const uint64_t f = ok ? T[x & 0xFFFFu] : 0ull;
+                  ovf |= __umul64hi(f, hc) != 0;
+                  const uint64_t fh = f * hc;
+                  v += fh;
+                  ovf |= v < fh;
+                }
               }
+              updl += v != 0;
               if (A.pout_kind == 2) {
                 A.pout[static_cast<uint64_t>(o ? sba : sab) * A.rsop + c * A.Poutp + i] = v;
               } else if (v) {
