@@ -152,3 +152,77 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
   for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(0xffffffffu, upd, o);
   if ((threadIdx.x & 31) == 0 && upd) atomicAdd(A.updates, static_cast<u64>(upd));
 }
+
+// First leaf level (no child tables on either end): the row of x is, per
+// colouring, the colour histogram of x's neighbours without x's own colour —
+// entry of colour d is d - [d > chi x] (the squeezed rank of {d}).  For light
+// vertices (degree <= 256, k <= 8) a thread owns one vertex and counts all
+// colourings in registers: 4-bit fields (k <= 8 colours in one word) flushed
+// every 12 neighbours into 16-bit fields, as in the 3-cycle histograms.  No
+// shared memory, no atomics; vertices arrive in degree order, so a warp's
+// rows have similar lengths.
+__global__ void __launch_bounds__(256) leaf_hist_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist,
+                                                        uint32_t nv) {
+  const uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x;
+  uint64_t upd = 0;
+  if (gi < nv) {
+    const uint32_t x = vlist[gi];
+    uint32_t N[kChiStride], H[kChiStride][4];
+#pragma unroll
+    for (int c = 0; c < kChiStride; ++c) {
+      N[c] = 0;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) H[c][w] = 0;
+    }
+    auto flush = [&]() {
+#pragma unroll
+      for (int c = 0; c < kChiStride; ++c) {
+        const uint32_t ev = N[c] & 0x0F0F0F0Fu, od = (N[c] >> 4) & 0x0F0F0F0Fu;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) H[c][w] += ((ev >> (8 * w)) & 0xFFu) | (((od >> (8 * w)) & 0xFFu) << 16);
+        N[c] = 0;
+      }
+    };
+    const uint64_t base = A.off[x], end = A.off[x + 1];
+    int pend = 0;
+    // 16-byte loads of the row (adj is padded by 16 bytes on upload)
+    for (uint64_t p = base & ~3ull; p < end; p += 4) {
+      const uint4 q = __ldg(reinterpret_cast<const uint4*>(A.adj + p));
+      const uint32_t ws[4] = {q.x, q.y, q.z, q.w};
+      uint64_t cw[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) cw[u] = (p + u >= base && p + u < end) ? load_colors(A.chi, ws[u]) : ~0ull;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (cw[u] == ~0ull) continue;
+        const uint32_t lo32 = static_cast<uint32_t>(cw[u]), hi32 = static_cast<uint32_t>(cw[u] >> 32);
+#pragma unroll
+        for (int c = 0; c < kChiStride; ++c) {
+          const uint32_t half = c < 4 ? lo32 : hi32;
+          N[c] += 1u << (((half >> (8 * (c & 3))) & 7u) << 2);
+        }
+      }
+      if (++pend == 3) {
+        flush();
+        pend = 0;
+      }
+    }
+    flush();
+    const uint64_t cxs = load_colors(A.chi, x);
+    uint64_t* orow = A.out + static_cast<uint64_t>(x) * A.rso;
+#pragma unroll
+    for (int c = 0; c < kChiStride; ++c) {
+      if (c >= A.C) break;
+      const uint32_t cx = color_of(cxs, c);
+#pragma unroll
+      for (int d = 0; d < 8; ++d) {
+        if (d >= A.k || d == static_cast<int>(cx)) continue;
+        const uint32_t v = (H[c][d >> 1] >> (16 * (d & 1))) & 0xFFFFu;
+        orow[c * A.Pout + d - (d > static_cast<int>(cx) ? 1 : 0)] = v;
+        upd += v != 0;
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(0xffffffffu, upd, o);
+  if ((threadIdx.x & 31) == 0 && upd) atomicAdd(A.updates, static_cast<u64>(upd));
+}
