@@ -36,15 +36,19 @@ __device__ __forceinline__ uint32_t leaf_map_size(const LeafMapArgs& A) {
   return static_cast<uint32_t>(A.k) * A.k * (A.ub ? A.Pb : 1u);
 }
 
-template <int GROUP>
+// Acc: the shared-memory accumulator type — uint32_t when the host's entry
+// bound (maxdeg^(s-1)) is below 2^32 (native 32-bit shared atomics, half the
+// banks), else u64 (checked unless the bound is below 2^62).
+template <int GROUP, class Acc>
 __global__ void __launch_bounds__(256)
 leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) {
+  constexpr bool k32 = sizeof(Acc) == 4;
   extern __shared__ u64 lsm[];
   const int kThreads = blockDim.x;
   const int kGroups = kThreads / GROUP;
   const uint32_t msize = leaf_map_size(A);
   uint16_t* map = reinterpret_cast<uint16_t*>(lsm);
-  u64* acc = lsm + (msize * 2 + 7) / 8;
+  Acc* acc = reinterpret_cast<Acc*>(lsm + (msize * 2 + 7) / 8);
   const uint32_t pb = A.ub ? A.Pb : 1u;
   for (uint32_t i = threadIdx.x; i < msize; i += kThreads) {
     const uint32_t ib = i % pb, cy = (i / pb) % A.k, cx = i / (pb * A.k);
@@ -62,10 +66,10 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
   // a CTA-sized group keeps one accumulator copy per warp (no cross-warp
   // contention on the same counters) and sums the copies at the end
   constexpr int kWarpsPerGroup = GROUP / 32;
-  u64* Zg = acc + static_cast<size_t>(g) * gstride * kWarpsPerGroup;
-  u64* Z = Zg;                      // [C][PZ] then [C][Pout]: the reduced copy
-  u64* Zw = Zg + (lane / 32) * gstride;  // this warp's copy
-  u64* O = Z + A.C * A.PZ;
+  Acc* Zg = acc + static_cast<size_t>(g) * gstride * kWarpsPerGroup;
+  Acc* Z = Zg;                      // [C][PZ] then [C][Pout]: the reduced copy
+  Acc* Zw = Zg + (lane / 32) * gstride;  // this warp's copy
+  Acc* O = Z + A.C * A.PZ;
   uint64_t upd = 0;
   const bool cpow2 = (A.C & (A.C - 1)) == 0;  // full batches: C = 8
   const int clog = __ffs(A.C) - 1;
@@ -85,11 +89,11 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
       const uint32_t y = __ldg(A.adj + base + j);
       const uint32_t cx = color_of(cxs, c), cy = A.chi[static_cast<uint64_t>(y) * kChiStride + c];
       const uint16_t* my = map + (cx * A.k + cy) * pb;
-      u64* Zc = Zw + c * A.PZ;
+      Acc* Zc = Zw + c * A.PZ;
       if (!A.ub) {
         const uint16_t t = my[0];
         if (t != 0xFFFF) {
-          atomicAdd(Zc + t, 1ull);
+          atomicAdd(Zc + t, static_cast<Acc>(1));
           ++upd;
         }
         continue;
@@ -106,8 +110,8 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
           if (!r[u]) continue;
           const uint16_t t = my[i0 + u];
           if (t == 0xFFFF) continue;
-          if (A.unchecked) atomicAdd(Zc + t, static_cast<u64>(r[u]));
-          else atomic_add_ck(Zc + t, r[u], A.err);
+          if (k32 || A.unchecked) atomicAdd(Zc + t, static_cast<Acc>(r[u]));
+          else atomic_add_ck(reinterpret_cast<u64*>(Zc + t), r[u], A.err);
           ++upd;
         }
       }
@@ -118,14 +122,15 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
       __syncthreads();
       for (uint32_t i = lane; i < A.C * A.PZ; i += GROUP) {
         uint64_t s = Zg[i];
-        for (int w = 1; w < kWarpsPerGroup; ++w) s = A.unchecked ? s + Zg[w * gstride + i] : add_ck(s, Zg[w * gstride + i], A.err);
-        Z[i] = s;
+        for (int w = 1; w < kWarpsPerGroup; ++w)
+          s = (k32 || A.unchecked) ? s + Zg[w * gstride + i] : add_ck(s, Zg[w * gstride + i], A.err);
+        Z[i] = static_cast<Acc>(s);
       }
       __syncthreads();
     }
     uint64_t* orow = A.out + static_cast<uint64_t>(x) * A.rso;
     if (!A.ua) {
-      for (uint32_t i = lane; i < A.C * A.Pout; i += GROUP) orow[i] = Z[i];
+      for (uint32_t i = lane; i < A.C * A.Pout; i += GROUP) orow[i] = static_cast<uint64_t>(Z[i]);
     } else {
       const uint64_t per = static_cast<uint64_t>(A.PZ) * A.Pa;
       for (uint64_t it = lane; it < per * A.C; it += GROUP) {
@@ -140,12 +145,13 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
         const uint32_t Mz = sig_expand(sig_unrank(c_lut, A.sZ - 1, iz), fx);
         const uint32_t Ma = sig_expand(sig_unrank(c_lut, A.sa - 1, ia), fx);
         if ((Mz & Ma) != fx) continue;
-        if (A.unchecked) atomicAdd(O + c * A.Pout + sig_index(c_lut, Mz | Ma, fx), static_cast<u64>(z * a));
-        else atomic_add_ck(O + c * A.Pout + sig_index(c_lut, Mz | Ma, fx), mul_ck(z, a, A.err), A.err);
+        if (k32 || A.unchecked) atomicAdd(O + c * A.Pout + sig_index(c_lut, Mz | Ma, fx), static_cast<Acc>(z * a));
+        else atomic_add_ck(reinterpret_cast<u64*>(O + c * A.Pout + sig_index(c_lut, Mz | Ma, fx)), mul_ck(z, a, A.err),
+                           A.err);
         ++upd;
       }
       if (GROUP == 32) __syncwarp(); else __syncthreads();
-      for (uint32_t i = lane; i < A.C * A.Pout; i += GROUP) orow[i] = O[i];
+      for (uint32_t i = lane; i < A.C * A.Pout; i += GROUP) orow[i] = static_cast<uint64_t>(O[i]);
     }
     if (GROUP == 32) __syncwarp(); else __syncthreads();
   }
