@@ -297,7 +297,8 @@ struct TriHistArgs {
   const uint32_t* rev;
   const uint8_t* chi;   // [n][kChiStride]
   int k, C;
-  int lane_mode;            // 1: lane per edge, register counters (k <= 8, lists < 65536)
+  int lane_mode;
+  int f_safe;               // host bound: every factor entry < 2^44 (lane mode: unchecked terms)            // 1: lane per edge, register counters (k <= 8, lists < 65536)
   const uint32_t* eorder;   // oriented edges in CN-length order (lane_mode)
   // stage 1: this block
   int s_out;
@@ -521,7 +522,6 @@ __global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_hist_kernel(
               for (uint32_t i = 0; i < A.P2; ++i) tbuf[o * A.P2 + i] = 0;
             continue;
           }
-          uint64_t fmax = 0;  // OR of the staged factors: decides the unchecked path
           if (PF) {
             // stage this orientation's factor row: independent loads in
             // flight together instead of one dependent gather per term
@@ -535,16 +535,13 @@ __global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_hist_kernel(
               for (int u = 0; u < 8; ++u) r[u] = i0 + u < PF ? __ldg(F + i0 + u) : 0ull;
 #pragma unroll
               for (int u = 0; u < 8; ++u)
-                if (i0 + u < PF) {
-                  fst[i0 + u] = r[u];
-                  fmax |= r[u];
-                }
+                if (i0 + u < PF) fst[i0 + u] = r[u];
             }
           }
           const u64* Fs = PF ? fst : nullptr;
           // lane-mode counters are < 2^16 and there are <= 15 terms: with every
-          // factor < 2^44 no product or partial sum can reach 2^64
-          const bool safe = LANE && (fmax >> 44) == 0;
+          // factor < 2^44 (host bound) no product or partial sum can reach 2^64
+          const bool safe = LANE && A.f_safe;
           const uint32_t tb = (c0 * k + c1) * A.P2;
           for (uint32_t i = 0; i < A.P2; ++i) {
             const uint32_t* tt = terms + static_cast<size_t>(tb + i) * A.nterm;
