@@ -27,6 +27,7 @@ struct LeafMapArgs {
   uint32_t rsb, rsa, rso;  // row strides (C_alloc * P)
   int sb, sa, sZ, k, C;
   int unchecked;  // entries provably < 2^62 (host bound): plain adds
+  int ub_n, ua_n, out_n;  // narrow (u32) tables, see bind()
   uint64_t* out;
   int* err;
   u64* updates;
@@ -99,12 +100,19 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
         continue;
       }
       if (cy == cx) continue;
-      const uint64_t* row = A.ub + static_cast<uint64_t>(y) * A.rsb + c * pb;
+      const uint64_t roff = static_cast<uint64_t>(y) * A.rsb + c * pb;
+      const uint64_t* row = A.ub + roff;
+      const uint32_t* row32 = reinterpret_cast<const uint32_t*>(A.ub) + roff;
       for (uint32_t i0 = 0; i0 < pb; i0 += 8) {
         // the row's loads are issued together, then consumed
         uint64_t r[8];
+        if (A.ub_n) {
 #pragma unroll
-        for (int u = 0; u < 8; ++u) r[u] = i0 + u < pb ? __ldg(row + i0 + u) : 0ull;
+          for (int u = 0; u < 8; ++u) r[u] = i0 + u < pb ? __ldg(row32 + i0 + u) : 0u;
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) r[u] = i0 + u < pb ? __ldg(row + i0 + u) : 0ull;
+        }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           if (!r[u]) continue;
@@ -130,7 +138,11 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
     }
     uint64_t* orow = A.out + static_cast<uint64_t>(x) * A.rso;
     if (!A.ua) {
-      for (uint32_t i = lane; i < A.C * A.Pout; i += GROUP) orow[i] = static_cast<uint64_t>(Z[i]);
+      if (A.out_n)
+        for (uint32_t i = lane; i < A.C * A.Pout; i += GROUP)
+          reinterpret_cast<uint32_t*>(A.out)[static_cast<uint64_t>(x) * A.rso + i] = static_cast<uint32_t>(Z[i]);
+      else
+        for (uint32_t i = lane; i < A.C * A.Pout; i += GROUP) orow[i] = static_cast<uint64_t>(Z[i]);
     } else {
       const uint64_t per = static_cast<uint64_t>(A.PZ) * A.Pa;
       for (uint64_t it = lane; it < per * A.C; it += GROUP) {
@@ -139,7 +151,8 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
         const uint32_t iz = static_cast<uint32_t>(r / A.Pa), ia = static_cast<uint32_t>(r - iz * A.Pa);
         const uint64_t z = Z[c * A.PZ + iz];
         if (!z) continue;
-        const uint64_t a = __ldg(A.ua + static_cast<uint64_t>(x) * A.rsa + c * A.Pa + ia);
+        const uint64_t aoff = static_cast<uint64_t>(x) * A.rsa + c * A.Pa + ia;
+        const uint64_t a = A.ua_n ? __ldg(reinterpret_cast<const uint32_t*>(A.ua) + aoff) : __ldg(A.ua + aoff);
         if (!a) continue;
         const uint32_t fx = 1u << color_of(cxs, c);
         const uint32_t Mz = sig_expand(sig_unrank(c_lut, A.sZ - 1, iz), fx);
@@ -151,7 +164,11 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
         ++upd;
       }
       if (GROUP == 32) __syncwarp(); else __syncthreads();
-      for (uint32_t i = lane; i < A.C * A.Pout; i += GROUP) orow[i] = static_cast<uint64_t>(O[i]);
+      if (A.out_n)
+        for (uint32_t i = lane; i < A.C * A.Pout; i += GROUP)
+          reinterpret_cast<uint32_t*>(A.out)[static_cast<uint64_t>(x) * A.rso + i] = static_cast<uint32_t>(O[i]);
+      else
+        for (uint32_t i = lane; i < A.C * A.Pout; i += GROUP) orow[i] = static_cast<uint64_t>(O[i]);
     }
     if (GROUP == 32) __syncwarp(); else __syncthreads();
   }
@@ -224,7 +241,9 @@ __global__ void __launch_bounds__(256) leaf_hist_kernel(LeafMapArgs A, const uin
       for (int d = 0; d < 8; ++d) {
         if (d >= A.k || d == static_cast<int>(cx)) continue;
         const uint32_t v = (H[c][d >> 1] >> (16 * (d & 1))) & 0xFFFFu;
-        orow[c * A.Pout + d - (d > static_cast<int>(cx) ? 1 : 0)] = v;
+        const uint32_t col = c * A.Pout + d - (d > static_cast<int>(cx) ? 1 : 0);
+        if (A.out_n) reinterpret_cast<uint32_t*>(A.out)[static_cast<uint64_t>(x) * A.rso + col] = v;
+        else orow[col] = v;
         upd += v != 0;
       }
     }

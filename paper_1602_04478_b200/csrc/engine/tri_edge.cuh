@@ -298,7 +298,8 @@ struct TriHistArgs {
   const uint8_t* chi;   // [n][kChiStride]
   int k, C;
   int lane_mode;
-  int f_safe;               // host bound: every factor entry < 2^44 (lane mode: unchecked terms)            // 1: lane per edge, register counters (k <= 8, lists < 65536)
+  int f_safe;               // host bound: every factor entry < 2^44 (lane mode: unchecked terms)
+  int F_n;                  // pivot factor stored narrow (u32)            // 1: lane per edge, register counters (k <= 8, lists < 65536)
   const uint32_t* eorder;   // oriented edges in CN-length order (lane_mode)
   // stage 1: this block
   int s_out;
@@ -525,14 +526,21 @@ __global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_hist_kernel(
           if (PF) {
             // stage this orientation's factor row: independent loads in
             // flight together instead of one dependent gather per term
-            const uint64_t* F;
-            if (A.fkind == 1) F = A.F + static_cast<uint64_t>(o ? b : a) * A.rsF + c * A.PF;
-            else if (A.fkind == 2) F = A.F + static_cast<uint64_t>(o ? a : b) * A.rsF + c * A.PF;
-            else F = A.F + static_cast<uint64_t>((o == 0) != (A.sw01 != 0) ? sab : sba) * A.rsF + c * A.PF;
+            uint64_t fo;
+            if (A.fkind == 1) fo = static_cast<uint64_t>(o ? b : a) * A.rsF + c * A.PF;
+            else if (A.fkind == 2) fo = static_cast<uint64_t>(o ? a : b) * A.rsF + c * A.PF;
+            else fo = static_cast<uint64_t>((o == 0) != (A.sw01 != 0) ? sab : sba) * A.rsF + c * A.PF;
+            const uint64_t* F = A.F + fo;
+            const uint32_t* F32 = reinterpret_cast<const uint32_t*>(A.F) + fo;
             for (uint32_t i0 = 0; i0 < PF; i0 += 8) {
               uint64_t r[8];
+              if (A.F_n) {
 #pragma unroll
-              for (int u = 0; u < 8; ++u) r[u] = i0 + u < PF ? __ldg(F + i0 + u) : 0ull;
+                for (int u = 0; u < 8; ++u) r[u] = i0 + u < PF ? __ldg(F32 + i0 + u) : 0u;
+              } else {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) r[u] = i0 + u < PF ? __ldg(F + i0 + u) : 0ull;
+              }
 #pragma unroll
               for (int u = 0; u < 8; ++u)
                 if (i0 + u < PF) fst[i0 + u] = r[u];
