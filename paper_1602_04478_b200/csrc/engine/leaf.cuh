@@ -71,7 +71,7 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
   Acc* Z = Zg;                      // [C][PZ] then [C][Pout]: the reduced copy
   Acc* Zw = Zg + (lane / 32) * gstride;  // this warp's copy
   Acc* O = Z + A.C * A.PZ;
-  uint64_t upd = 0;
+  uint32_t upd = 0;  // per-thread contribution count (dp_updates)
   const bool cpow2 = (A.C & (A.C - 1)) == 0;  // full batches: C = 8
   const int clog = __ffs(A.C) - 1;
   for (uint32_t gi = blockIdx.x * kGroups + g; gi < nv; gi += gridDim.x * kGroups) {
