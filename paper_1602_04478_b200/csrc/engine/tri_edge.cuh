@@ -384,7 +384,10 @@ __device__ __forceinline__ void build_terms(uint32_t* terms, uint16_t* idx1, int
 #define MB_TRI_MINB 2  // resident CTAs per SM the register budget is sized for (126 regs, no spill;
                        // measured: 3 -> 80 regs + spills, 13.4 ms vs 11.3 ms per 3 batches)
 #endif
-template <bool LANE>
+// LANE: lane-per-edge register histograms (k <= 8, lists < 65536).
+// NARROW: the pivot factor is a narrow (u32) table on the unchecked path, so it
+// is staged as u32 and each term is one 32x32->64 multiply-add.
+template <bool LANE, bool NARROW>
 __global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_hist_kernel(TriHistArgs A) {
   extern __shared__ uint32_t hsm[];
   const int k = A.k, C = A.C;
@@ -403,6 +406,7 @@ __global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_hist_kernel(
   uint32_t* hist = wbase + static_cast<size_t>(wid) * (L.hist_per_warp + L.tbuf_per_warp + L.fst_per_warp);
   u64* tbuf = reinterpret_cast<u64*>(hist + L.hist_per_warp) + static_cast<size_t>(lane) * (2 * A.P2 + 1);
   u64* fst = reinterpret_cast<u64*>(hist + L.hist_per_warp + L.tbuf_per_warp) + static_cast<size_t>(lane) * (PF | 1u);
+  uint32_t* fst32 = reinterpret_cast<uint32_t*>(fst);
   uint16_t* hist16 = reinterpret_cast<uint16_t*>(hist);
   uint32_t ovf = 0;  // overflow seen by this thread (one atomic at exit)
   uint64_t local[kChiStride];
@@ -532,7 +536,16 @@ __global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_hist_kernel(
             else fo = static_cast<uint64_t>((o == 0) != (A.sw01 != 0) ? sab : sba) * A.rsF + c * A.PF;
             const uint64_t* F = A.F + fo;
             const uint32_t* F32 = reinterpret_cast<const uint32_t*>(A.F) + fo;
-            for (uint32_t i0 = 0; i0 < PF; i0 += 8) {
+            if (NARROW) {
+              for (uint32_t i0 = 0; i0 < PF; i0 += 8) {
+                uint32_t r[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) r[u] = i0 + u < PF ? __ldg(F32 + i0 + u) : 0u;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                  if (i0 + u < PF) fst32[i0 + u] = r[u];
+              }
+            } else for (uint32_t i0 = 0; i0 < PF; i0 += 8) {
               uint64_t r[8];
               if (A.F_n) {
 #pragma unroll
@@ -556,7 +569,16 @@ __global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_hist_kernel(
             uint64_t v = 0;
             // branch-free multiply-add: lanes of a warp hold different
             // colour pairs, so per-term zero tests would only diverge
-            if (safe) {
+            if (NARROW) {
+#pragma unroll 4
+              for (int t = 0; t < A.nterm; ++t) {
+                const uint32_t x = tt[t];
+                const bool ok = x != ~0u;
+                const uint32_t hc = ok ? hval(x >> 16) : 0u;
+                const uint32_t f = ok ? fst32[x & 0xFFFFu] : 0u;
+                v += static_cast<uint64_t>(f) * hc;
+              }
+            } else if (safe) {
 #pragma unroll 4
               for (int t = 0; t < A.nterm; ++t) {
                 const uint32_t x = tt[t];
