@@ -351,14 +351,27 @@ unsigned grid_for(uint64_t work, unsigned block) {
 
 // Sort keys for the CN-length edge order: ~length so an ascending sort yields
 // decreasing lengths.
-__global__ void k_cn_len_keys(const uint64_t* __restrict__ cn_off, uint64_t nout, uint32_t* __restrict__ keys,
-                              uint32_t* __restrict__ vals, u64* __restrict__ nonempty) {
+// Sort key of oriented edge j for the lane-per-edge histogram kernels:
+// decreasing CN-length bucket (quarter octaves, so a warp's 32 lists are
+// within ~25% of each other), then j itself — oriented edges are stored by
+// source vertex, so lanes of a warp share sources and their factor rows.
+__global__ void k_cn_len_keys(const uint64_t* __restrict__ cn_off, uint64_t nout, uint64_t* __restrict__ keys,
+                              uint32_t* __restrict__ vals, u64* __restrict__ nonempty,
+                              unsigned* __restrict__ maxlen) {
   const uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   const uint64_t len = j < nout ? cn_off[j + 1] - cn_off[j] : 0;
   const unsigned nz = __ballot_sync(0xffffffffu, len > 0);
   if ((threadIdx.x & 31) == 0 && nz) atomicAdd(nonempty, static_cast<u64>(__popc(nz)));
   if (j >= nout) return;
-  keys[j] = ~static_cast<uint32_t>(len > 0xFFFFFFFFull ? 0xFFFFFFFFull : len);
+  const uint32_t l = static_cast<uint32_t>(len > 0xFFFFFFFFull ? 0xFFFFFFFFull : len);
+  if (l) atomicMax(maxlen, l);
+  uint32_t bucket = 0;  // 0 for empty lists: sorted last
+  if (l) {
+    const uint32_t b = 31 - __clz(l);
+    const uint32_t frac = b >= 2 ? (l >> (b - 2)) & 3u : (l << (2 - b)) & 3u;
+    bucket = 1 + 4 * b + frac;
+  }
+  keys[j] = (static_cast<uint64_t>(0xFFu - bucket) << 32) | static_cast<uint32_t>(j);
   vals[j] = static_cast<uint32_t>(j);
 }
 
