@@ -40,7 +40,10 @@ __device__ __forceinline__ uint32_t leaf_map_size(const LeafMapArgs& A) {
 // Acc: the shared-memory accumulator type — uint32_t when the host's entry
 // bound (maxdeg^(s-1)) is below 2^32 (native 32-bit shared atomics, half the
 // banks), else u64 (checked unless the bound is below 2^62).
-template <int GROUP, class Acc>
+// PB: the child row length when it is a compile-time constant (common query
+// shapes: 4, 5, 6, 10), else 0 = read from A.Pb — a constant row unrolls the
+// loads and the consume loop exactly (no guarded 8-wide chunks).
+template <int GROUP, class Acc, int PB>
 __global__ void __launch_bounds__(256)
 leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) {
   constexpr bool k32 = sizeof(Acc) == 4;
@@ -50,7 +53,7 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
   const uint32_t msize = leaf_map_size(A);
   uint16_t* map = reinterpret_cast<uint16_t*>(lsm);
   Acc* acc = reinterpret_cast<Acc*>(lsm + (msize * 2 + 7) / 8);
-  const uint32_t pb = A.ub ? A.Pb : 1u;
+  const uint32_t pb = PB ? static_cast<uint32_t>(PB) : (A.ub ? A.Pb : 1u);
   for (uint32_t i = threadIdx.x; i < msize; i += kThreads) {
     const uint32_t ib = i % pb, cy = (i / pb) % A.k, cx = i / (pb * A.k);
     uint16_t t = 0xFFFF;
