@@ -46,13 +46,13 @@ CONFIGS = {
             query=[(0, 1), (1, 2), (2, 0), (1, 3), (3, 2), (2, 4), (4, 5)], seeds=list(range(100, 108)),
             sample_n=20_000),
     2: dict(name="rmat22_c7", gen=("rmat", 22, 16, 3), k=7, query=[(i, (i + 1) % 7) for i in range(7)],
-            seeds=list(range(200, 216)), sample_n=None),
+            seeds=list(range(200, 216)), sample_n=10),  # sample: R-MAT scale 10
     3: dict(name="chunglu4m_theta8", gen=("cl", 4_000_000, 2.3, 20.0, 4), k=8,
             query=[(0, 1), (1, 2), (2, 7), (0, 3), (3, 4), (4, 7), (0, 5), (5, 6), (6, 7)],
-            seeds=list(range(300, 316)), sample_n=None),
+            seeds=list(range(300, 316)), sample_n=500),
     4: dict(name="chunglu2m_sp10", gen=("cl", 2_000_000, 2.1, 24.0, 5), k=10,
             query=[(0, 1), (1, 2), (2, 3), (3, 4), (4, 5), (5, 0), (0, 2), (3, 5), (1, 6), (6, 7), (7, 8),
-                   (8, 9), (9, 1)], seeds=list(range(400, 464)), sample_n=None),
+                   (8, 9), (9, 1)], seeds=list(range(400, 464)), sample_n=600),
 }
 
 
@@ -68,7 +68,7 @@ def make_graph(mb, gen, n_override=None):
         n, gamma, avg, seed = gen[1:]
         return mb.DataGraph.chung_lu(n_override or n, gamma, avg, seed)
     scale, ef, seed = gen[1:]
-    return mb.DataGraph.rmat(scale, ef, 0.57, 0.19, 0.19, seed)
+    return mb.DataGraph.rmat(n_override or scale, ef, 0.57, 0.19, 0.19, seed)
 
 
 class ClockSampler:
@@ -182,7 +182,8 @@ def reference_arm(args, cfg, ws, rank):
     R = Reference()
     rg = R.graph(g.num_vertices(), g.edges())
     rp = R.plan(cfg["k"], cfg["query"])
-    chis = np.stack([rg.coloring(cfg["k"], s) for s in cfg["seeds"]])
+    seeds = cfg["seeds"][:16]  # bounded sample: at most 16 colourings per step (one per host core)
+    chis = np.stack([rg.coloring(cfg["k"], s) for s in seeds])
     threads, workers = ref_layout(len(chis))
     for _ in range(args.warmup):
         R.count_batch(rg, rp, chis[: min(len(chis), threads)], engine=1, threads=threads, workers=workers)
@@ -190,14 +191,14 @@ def reference_arm(args, cfg, ws, rank):
     for _ in range(args.steps):
         R.count_batch(rg, rp, chis, engine=1, threads=threads, workers=workers)
     dt = (time.perf_counter() - t0) / args.steps
-    v = len(cfg["seeds"]) / dt
+    v = len(seeds) / dt
     sample = (f"{cfg['name']} generator at n={g.num_vertices()} (m={g.num_edges()}), same query/k/seeds; "
-              f"{len(cfg['seeds'])} colourings per step, {threads} at a time x {workers} BSP workers each")
+              f"{len(seeds)} colourings per step, {threads} at a time x {workers} BSP workers each")
     print(json.dumps({
         "impl": "reference", "metric": "colorings/sec", "value": v, "unit": "colorings/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": cfg["name"], "sample_n": g.num_vertices(), "colorings_per_step": len(cfg["seeds"])},
+        "config": {"workload": cfg["name"], "sample_n": g.num_vertices(), "colorings_per_step": len(seeds)},
         "cpu_baseline": {"value": v, "unit": "colorings/s", "cores": threads * workers,
                          "kind": "reference", "sample": sample},
         "e2e": {"value": v, "unit": "colorings/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -215,15 +216,15 @@ def cpu_baseline(cfg):
     R = Reference()
     rg = R.graph(g.num_vertices(), g.edges())
     rp = R.plan(cfg["k"], cfg["query"])
-    chis = np.stack([rg.coloring(cfg["k"], s) for s in cfg["seeds"]])
+    chis = np.stack([rg.coloring(cfg["k"], s) for s in cfg["seeds"][:16]])
     threads, workers = ref_layout(len(chis))
     t0 = time.perf_counter()
     R.count_batch(rg, rp, chis, engine=1, threads=threads, workers=workers)
     dt = time.perf_counter() - t0
-    return {"value": len(cfg["seeds"]) / dt, "unit": "colorings/s", "cores": threads * workers,
+    return {"value": len(chis) / dt, "unit": "colorings/s", "cores": threads * workers,
             "kind": "reference",
             "sample": (f"compiled reference (oracle/_ref, DB engine) on the {cfg['name']} generator at "
-                       f"n={g.num_vertices()} (m={g.num_edges()}): {len(cfg['seeds'])} colourings in {dt:.1f}s, "
+                       f"n={g.num_vertices()} (m={g.num_edges()}): {len(chis)} colourings in {dt:.1f}s, "
                        f"{threads} colourings at a time x {workers} BSP workers each")}
 
 
@@ -234,7 +235,7 @@ def our_arm(args, cfg, ws, rank, local):
 
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
-    g = make_graph(mb, cfg["gen"])
+    g = make_graph(mb, cfg["gen"], args.size)
     plan = mb.QueryPlan(cfg["k"], cfg["query"])
     k, n = cfg["k"], g.num_vertices()
     # weak scaling: rank r counts its own batch (seed offset r * batch)
@@ -317,7 +318,8 @@ def our_arm(args, cfg, ws, rank, local):
         "metric": "colorings/sec", "value": value, "unit": "colorings/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": cfg["name"], "n": n, "m": g.num_edges(), "k": k, "colorings_per_step": nb,
+        "config": {"workload": cfg["name"] + (f"@size{args.size}" if args.size else ""), "n": n, "m": g.num_edges(),
+                   "k": k, "colorings_per_step": nb,
                    "query_edges": cfg["query"], "parallelism": f"colorings sharded over {ws} GPU(s)",
                    "l2": "flushed between steps (256 MB write) and working set > L2",
                    "graph_prep_ms": prep_ms, "first_call_s": first_call_s},
@@ -348,6 +350,9 @@ def main():
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--size", type=int, default=None,
+                    help="override the generator size (n, or the R-MAT scale): supplementary reduced runs of "
+                         "configs 2-4, whose full sizes exceed u64 counts or HBM (DESIGN.md)")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     ws, rank, local = dist_setup(args)

@@ -500,7 +500,8 @@ struct CycleRunner {
   int* err;
   u64* scalar;
   u64* upd;
-  std::function<void(const char*, const std::function<void()>&)> launch;
+  std::function<void(const char*, const std::function<void()>&, uint64_t)> launch_b;
+  void launch(const char* name, const std::function<void()>& f, uint64_t bytes = 0) { launch_b(name, f, bytes); }
   std::function<void(const uint64_t*, uint64_t*, uint64_t)> scan;  // exclusive scan of n+1
   DBuf sort_tmp;
   uint64_t mem_budget = 6ull << 30;  // bytes of per-hop scratch per batch
@@ -622,7 +623,10 @@ struct CycleRunner {
               (unsigned long long)in.n, (unsigned long long)W, in.s, in.P, (int)first, in.has_r, out.has_r,
               (int)record, out.s, out.P, (const void*)A.etab, A.Pe, A.se, A.rse, A.e_rev,
               (unsigned long long)A.n_etab, (const void*)A.ntab, A.Pn, A.sn, A.rsn, bits);
-    launch("cycle_hop_expand", [&] { k_hop_expand<<<grid_for(W, kHopTile), kHopTile, 0, stream>>>(A); });
+    // compulsory bytes: per item its neighbour id, colour, output key and
+    // row; per input entry its key, work offsets and row
+    const uint64_t hop_bytes = W * (4 + 1 + 8 + 8ull * out.P) + in.n * (8 + 16 + 8ull * in.P);
+    launch("cycle_hop_expand", [&] { k_hop_expand<<<grid_for(W, kHopTile), kHopTile, 0, stream>>>(A); }, hop_bytes);
     aggregate(keys, rows, W, out.P, out.key, out.pay, out.n, (out.has_r ? 3 : 2) * bits);
     return true;
   }
@@ -857,7 +861,7 @@ struct CycleRunner {
           cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &reserved);
           cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
         }
-        const uint64_t avail = fr + (reserved > used ? reserved - used : 0);
+        const uint64_t avail = fr + (reserved > used ? reserved - used : 0) + dbuf_cache().cached;
         mem_budget = std::min<uint64_t>(48ull << 30, std::max<uint64_t>(2ull << 30, avail / 4));
       }
       static const char* mb_env = std::getenv("MB_CYCLE_BUDGET_MB");
@@ -875,6 +879,7 @@ struct CycleRunner {
     uint64_t ok = 0, failed = 0;
     const auto t_solve = std::chrono::steady_clock::now();
     wait_s = 0;
+    t_dbuf_alloc_s = 0;
     for (int h = 0; h < nh; ++h) {
       uint32_t bs = first_batch, cap = first_batch;  // cap: below the last size that failed
       for (uint32_t x0 = 0; x0 < G.n;) {
@@ -896,8 +901,9 @@ struct CycleRunner {
     if (dbg) {
       MB_CUDA(cudaStreamSynchronize(stream));
       const double tot = std::chrono::duration<double>(std::chrono::steady_clock::now() - t_solve).count();
-      fprintf(stderr, "cycle L=%d: %llu batches, %llu discarded attempts, budget %.1f GB, %.3f s (%.3f s in d2h)\n",
-              C.L, (unsigned long long)ok, (unsigned long long)failed, mem_budget / 1e9, tot, wait_s);
+      fprintf(stderr, "cycle L=%d: %llu batches, %llu discarded attempts, budget %.1f GB, %.3f s (%.3f s in d2h, "
+              "%.3f s in allocation)\n", C.L, (unsigned long long)ok, (unsigned long long)failed, mem_budget / 1e9, tot,
+              wait_s, t_dbuf_alloc_s);
     }
   }
 

@@ -10,6 +10,7 @@
 #include <cstdlib>
 #include <functional>
 #include <map>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <thread>
@@ -38,6 +39,7 @@ using u64 = unsigned long long;
 // (StreamScope) and freed on the stream it was allocated on.  `persistent`
 // buffers (process-lifetime LUTs) use cudaMalloc.
 thread_local cudaStream_t t_dbuf_stream = nullptr;
+thread_local double t_dbuf_alloc_s = 0;  // host time in allocation calls (MB_DEBUG_BATCH)
 
 struct StreamScope {  // sets the allocation stream for the engine entry point's duration
   cudaStream_t prev;
@@ -45,8 +47,58 @@ struct StreamScope {  // sets the allocation stream for the engine entry point's
   ~StreamScope() { t_dbuf_stream = prev; }
 };
 
+// Freed device blocks are cached per stream and handed to later requests of
+// a similar size on the same stream (stream order makes the reuse safe):
+// cudaMallocAsync alone spent up to 1 s per cycle-engine solve re-mapping
+// pool memory (MB_DEBUG_BATCH).  Sizes are rounded to 64 KB (2 MB above
+// 64 MB) classes; a cached block serves requests up to 25 % smaller.
+struct DBufCache {
+  std::mutex mu;
+  std::map<cudaStream_t, std::multimap<size_t, void*>> blocks;
+  size_t cached = 0;
+  static constexpr size_t kCap = 64ull << 30;
+  static size_t round(size_t b) {
+    const size_t g = b > (64ull << 20) ? (2ull << 20) : (64ull << 10);
+    return (b + g - 1) / g * g;
+  }
+  void* take(cudaStream_t s, size_t b, size_t* got) {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = blocks.find(s);
+    if (it == blocks.end()) return nullptr;
+    auto jt = it->second.lower_bound(b);
+    if (jt == it->second.end() || jt->first > b + b / 4) return nullptr;
+    void* p = jt->second;
+    *got = jt->first;
+    cached -= jt->first;
+    it->second.erase(jt);
+    return p;
+  }
+  bool put(cudaStream_t s, size_t b, void* p) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (cached + b > kCap) return false;
+    blocks[s].emplace(b, p);
+    cached += b;
+    return true;
+  }
+  void clear(cudaStream_t s) {  // the stream is about to go away
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = blocks.find(s);
+    if (it == blocks.end()) return;
+    for (auto& kv : it->second) {
+      cudaFreeAsync(kv.second, s);
+      cached -= kv.first;
+    }
+    blocks.erase(it);
+  }
+};
+inline DBufCache& dbuf_cache() {
+  static DBufCache* c = new DBufCache;  // never destroyed: outlives static engines at exit
+  return *c;
+}
+
 struct DBuf {
   void* p = nullptr;
+  size_t cap = 0;  // bytes actually allocated (size class)
   size_t bytes = 0;
   cudaStream_t s = nullptr;
   bool persistent = false;
@@ -54,11 +106,13 @@ struct DBuf {
   explicit DBuf(size_t b) { alloc(b); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), bytes(o.bytes), s(o.s), persistent(o.persistent) { o.p = nullptr, o.bytes = 0; }
+  DBuf(DBuf&& o) noexcept : p(o.p), cap(o.cap), bytes(o.bytes), s(o.s), persistent(o.persistent) {
+    o.p = nullptr, o.bytes = 0, o.cap = 0;
+  }
   DBuf& operator=(DBuf&& o) noexcept {
     release();
-    p = o.p, bytes = o.bytes, s = o.s, persistent = o.persistent;
-    o.p = nullptr, o.bytes = 0;
+    p = o.p, cap = o.cap, bytes = o.bytes, s = o.s, persistent = o.persistent;
+    o.p = nullptr, o.bytes = 0, o.cap = 0;
     return *this;
   }
   ~DBuf() { release(); }
@@ -69,7 +123,16 @@ struct DBuf {
         MB_CUDA(cudaMalloc(&p, b));
       } else {
         s = t_dbuf_stream;
-        MB_CUDA(cudaMallocAsync(&p, b, s));
+        const auto t0 = std::chrono::steady_clock::now();
+        cap = DBufCache::round(b);
+        size_t got = 0;
+        p = dbuf_cache().take(s, cap, &got);
+        if (p) {
+          cap = got;  // a cached block may be larger than asked for
+        } else {
+          MB_CUDA(cudaMallocAsync(&p, cap, s));
+        }
+        t_dbuf_alloc_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       }
     }
     bytes = b;
@@ -77,10 +140,11 @@ struct DBuf {
   void release() {
     if (p) {
       if (persistent) cudaFree(p);
-      else cudaFreeAsync(p, s);
+      else if (!dbuf_cache().put(s, cap, p)) cudaFreeAsync(p, s);
     }
     p = nullptr;
     bytes = 0;
+    cap = 0;
   }
   template <class T>
   T* as() const {
