@@ -1,0 +1,397 @@
+// Histogram-path 3-cycle blocks in relative colour coordinates.  Included by
+// engine_host.inc after tri_edge.cuh (uses TriHistArgs and its helpers).
+//
+// Same work as tri_hist_kernel's lane mode (one lane per oriented edge, the
+// common neighbours' colours counted in registers for all colourings of the
+// batch), but the join is evaluated without per-term tables.  For a pivot
+// colour pair {c0, c1} every colour set the block touches contains both, so
+// it is a subset of the M = k - 2 remaining colours R = [k] \ {c0, c1} — and
+// indexing R by rank ("relative coordinates") makes the whole join static:
+//   stage 1  T[A] = sum_{r in A} h[r] * F'[A \ r]        |A| = s_out - 2
+//   stage 2  U[A] = sum_{r in A} h[r] * T[A \ r]          |A| = s_parent - 2
+// where h[r] is the histogram count of colour R[r] and F' the pivot factor's
+// entries restricted to R.  Each relative subset A ranks to the row index of
+// the squeezed colex layout (sig.cuh) directly for edge-keyed rows (the fixed
+// colours are exactly {c0, c1}), so subset lists, ranks and term structure are
+// compile-time constants and every product is a register multiply-add.  Only
+// three things still depend on the lane's colours: which histogram counts
+// form h (R[r] = r-th colour not in {c0, c1}), where a node factor keyed by one
+// pivot colour keeps its R-entries (a per-CTA byte map over (c_f, c_other)),
+// and the index of a unary output entry (the existing idx1 maps).
+//
+// Reference semantics: the same 3-cycle block evaluation by DB as
+// tri_hist_kernel (engine.cpp:353-366, table.cpp:255-476 for the joins).
+
+namespace canon {
+
+constexpr int cbinom(int n, int r) {
+  if (r < 0 || r > n) return 0;
+  int b = 1;
+  for (int i = 1; i <= r; ++i) b = b * (n - r + i) / i;
+  return b;
+}
+constexpr int cpopc(uint32_t x) {
+  int c = 0;
+  for (; x; x &= x - 1u) ++c;
+  return c;
+}
+// j-th t-subset of {0..m-1} in colex order (= increasing mask value)
+constexpr uint32_t nth_subset(int m, int t, int j) {
+  int cnt = 0;
+  for (uint32_t x = 0; x < (1u << m); ++x)
+    if (cpopc(x) == t) {
+      if (cnt == j) return x;
+      ++cnt;
+    }
+  return 0;
+}
+// colex rank among masks of the same popcount (sig_rank with constant binomials)
+constexpr int crank(uint32_t mask) {
+  int r = 0, i = 1;
+  for (int c = 0; c < 32; ++c)
+    if ((mask >> c) & 1u) r += cbinom(c, i++);
+  return r;
+}
+// the b-th set bit of mask (b counted from the lowest)
+constexpr int nth_bit(uint32_t mask, int b) {
+  for (int c = 0; c < 32; ++c)
+    if ((mask >> c) & 1u) {
+      if (b == 0) return c;
+      --b;
+    }
+  return -1;
+}
+
+template <class F, int... I>
+__device__ __forceinline__ void sfor_impl(F&& f, std::integer_sequence<int, I...>) {
+  (f(std::integral_constant<int, I>{}), ...);
+}
+// f(integral_constant<int, i>) for i = 0..N-1, fully expanded at compile time
+template <int N, class F>
+__device__ __forceinline__ void sfor(F&& f) {
+  sfor_impl(f, std::make_integer_sequence<int, N>{});
+}
+
+}  // namespace canon
+
+// Lane-mode register histogram of oriented edge j: H[c][w] holds the counts
+// of colours 2w and 2w+1 in colouring slot c as two 16-bit fields (lists are
+// shorter than 65536 in lane mode).  4-bit fields (all k <= 8 colours in one
+// word) are flushed into the 16-bit ones every 12 entries; the list is read
+// with 16-byte loads (cn_w is padded).
+__device__ __forceinline__ void lane_histogram(const TriHistArgs& A, uint64_t j, uint32_t (&H)[kChiStride][4]) {
+  uint32_t N[kChiStride];
+#pragma unroll
+  for (int c = 0; c < kChiStride; ++c) {
+    N[c] = 0;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) H[c][w] = 0;
+  }
+  auto flush = [&]() {
+#pragma unroll
+    for (int c = 0; c < kChiStride; ++c) {
+      const uint32_t ev = N[c] & 0x0F0F0F0Fu, od = (N[c] >> 4) & 0x0F0F0F0Fu;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) H[c][w] += ((ev >> (8 * w)) & 0xFFu) | (((od >> (8 * w)) & 0xFFu) << 16);
+      N[c] = 0;
+    }
+  };
+  const uint64_t lo_ = A.cn_off[j], hi_ = A.cn_off[j + 1];
+  int pend = 0;
+  for (uint64_t p = lo_ & ~3ull; p < hi_; p += 4) {
+    const uint4 q = __ldg(reinterpret_cast<const uint4*>(A.cn_w + p));
+    const uint32_t ws[4] = {q.x, q.y, q.z, q.w};
+    uint64_t cw[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool in = p + u >= lo_ && p + u < hi_;
+      cw[u] = in ? load_colors(A.chi, ws[u]) : ~0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (cw[u] == ~0ull) continue;
+      const uint32_t lo32 = static_cast<uint32_t>(cw[u]), hi32 = static_cast<uint32_t>(cw[u] >> 32);
+#pragma unroll
+      for (int c = 0; c < kChiStride; ++c) {
+        const uint32_t half = c < 4 ? lo32 : hi32;
+        N[c] += 1u << (((half >> (8 * (c & 3))) & 7u) << 2);
+      }
+    }
+    if (++pend == 3) {
+      flush();
+      pend = 0;
+    }
+  }
+  flush();
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+__device__ __forceinline__ void prefetch_span(const void* p, uint32_t bytes) {
+  const char* c = static_cast<const char*>(p);
+  for (uint32_t o = 0; o < bytes; o += 128) prefetch_l2(c + o);
+  prefetch_l2(c + bytes - 1);
+}
+
+// K colours; S1 = this block's s_out; FK = pivot factor kind (0 none, 1 node
+// at P0, 2 node at P1, 3 edge (P0, P1)); SP = the fused parent's s_out (0: not
+// fused); NARROW = node factor stored as u32.
+template <int K, int S1, int FK, int SP, bool NARROW>
+__global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_canon_kernel(TriHistArgs A) {
+  constexpr int M = K - 2;                       // |R|
+  constexpr int T1 = S1 - 2;                     // stage-1 subset size
+  constexpr int P2 = canon::cbinom(M, T1);       // stage-1 entries
+  constexpr int NB = FK ? canon::cbinom(M, T1 - 1) : 1;  // factor entries restricted to R
+  constexpr int TP = SP ? SP - 2 : 0;
+  constexpr int P2p = SP ? canon::cbinom(M, TP) : 0;
+  static_assert(K <= 8 && T1 >= 1 && (FK != 0 || T1 == 1), "shape");
+
+  extern __shared__ uint32_t hsm[];
+  // per-CTA maps: fmap[(cf*K + cx)*NB + j] = row index, in the node factor keyed
+  // by colour cf, of the j-th (T1-1)-subset of R = [K] \ {cf, cx};
+  // idx1/idx1p[(c0*K + c1)*P + i] = unary-output index of relative entry i
+  constexpr int FMAP = (FK == 1 || FK == 2) ? K * K * NB : 0;
+  uint8_t* fmap = reinterpret_cast<uint8_t*>(hsm);
+  uint16_t* idx1 = reinterpret_cast<uint16_t*>(hsm + (FMAP + 3) / 4);
+  const int n1 = A.out_kind == 1 ? K * K * P2 : 0;
+  uint16_t* idx1p = idx1 + n1;
+  const int n1p = (SP && A.pout_kind == 1) ? K * K * P2p : 0;
+  uint16_t* hist16_base = idx1p + n1p + ((n1 + n1p) & 1);  // 4-byte aligned
+  for (int e = threadIdx.x; e < K * K * (NB + P2 + P2p); e += blockDim.x) {
+    // one pass over (c0, c1, slot) triples fills whichever maps this launch needs
+    const int q = e / (K * K), pr = e % (K * K), c0 = pr / K, c1 = pr % K;
+    if (c0 == c1) continue;
+    const uint32_t f2 = (1u << c0) | (1u << c1);
+    if (q < NB) {
+      if (FMAP) {
+        const uint32_t S = sig_expand(sig_unrank(c_lut, T1 - 1, q), f2) & ~(1u << c1);
+        fmap[pr * NB + q] = static_cast<uint8_t>(sig_index(c_lut, S, 1u << c0));
+      }
+    } else if (q < NB + P2) {
+      const int i = q - NB;
+      if (n1) idx1[pr * P2 + i] = static_cast<uint16_t>(sig_index(c_lut, sig_expand(sig_unrank(c_lut, T1, i), f2), 1u << c0));
+    } else {
+      const int i = q - NB - P2;
+      if (n1p)
+        idx1p[pr * P2p + i] = static_cast<uint16_t>(sig_index(c_lut, sig_expand(sig_unrank(c_lut, TP, i), f2), 1u << c0));
+    }
+  }
+  __syncthreads();
+
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr uint32_t LS = 2 * ((((kChiStride * K) + 1) / 2) | 1u);  // u16 per edge row, odd word stride
+  uint16_t* hrow = hist16_base + static_cast<size_t>(threadIdx.x) * LS;
+  const int C = A.C;
+  uint32_t ovf = 0;
+  uint64_t local[kChiStride];
+#pragma unroll
+  for (int c = 0; c < kChiStride; ++c) local[c] = 0;
+  uint64_t upd = 0;
+  const uint64_t nbatch = (A.nitems + 31) / 32;
+  const uint32_t fbytes = FK ? static_cast<uint32_t>(C) * A.PF * (NARROW ? 4u : 8u) : 0u;
+  for (uint64_t bt = static_cast<uint64_t>(blockIdx.x) * kHistWarps + wid; bt < nbatch;
+       bt += static_cast<uint64_t>(gridDim.x) * kHistWarps) {
+    const uint64_t jj = bt * 32 + lane;
+    if (jj >= A.nitems) continue;
+    const uint64_t j = A.eorder[jj];
+    const uint32_t a = A.out_src[j], b = A.out_nbr[j];
+    const uint32_t sab = A.out_slot[j], sba = A.rev[sab];
+    // the pivot factor rows are gathered after the list scan: start their
+    // trip to L2 now
+    if (FK == 1 || FK == 2) {
+      const char* F = reinterpret_cast<const char*>(A.F);
+      const uint32_t rb = A.rsF * (NARROW ? 4u : 8u);
+      prefetch_span(F + static_cast<uint64_t>(a) * rb, fbytes);
+      prefetch_span(F + static_cast<uint64_t>(b) * rb, fbytes);
+    } else if (FK == 3) {
+      const char* F = reinterpret_cast<const char*>(A.F);
+      prefetch_span(F + static_cast<uint64_t>(sab) * A.rsF * 8u, fbytes);
+      prefetch_span(F + static_cast<uint64_t>(sba) * A.rsF * 8u, fbytes);
+    }
+    uint32_t H[kChiStride][4];
+    lane_histogram(A, j, H);
+#pragma unroll
+    for (int c = 0; c < kChiStride; ++c)
+#pragma unroll
+      for (int d = 0; d < 8; ++d)  // static indices keep H in registers
+        if (d < K) hrow[c * K + d] = static_cast<uint16_t>(H[c][d >> 1] >> (16 * (d & 1)));
+    const uint64_t cas = load_colors(A.chi, a), cbs = load_colors(A.chi, b);
+    uint32_t updl = 0;
+    for (int c = 0; c < C; ++c) {
+      const uint32_t ca = color_of(cas, c), cb = color_of(cbs, c);
+      if (ca == cb) {
+        // no colourful match on this edge: materialised edge rows are zero
+        if (A.out_kind == 2)
+          for (int o = 0; o < 2; ++o)
+            for (uint32_t i = 0; i < A.Pout; ++i) A.out[static_cast<uint64_t>(o ? sba : sab) * A.rso + c * A.Pout + i] = 0;
+        if (SP && A.pout_kind == 2)
+          for (int o = 0; o < 2; ++o)
+            for (uint32_t i = 0; i < A.Poutp; ++i)
+              A.pout[static_cast<uint64_t>(o ? sba : sab) * A.rsop + c * A.Poutp + i] = 0;
+        continue;
+      }
+      const uint32_t lo = min(ca, cb), hi = max(ca, cb);
+      // h[r] = count of the r-th colour not in {ca, cb}
+      uint32_t h[M];
+#pragma unroll
+      for (int r = 0; r < M; ++r) {
+        uint32_t d = r;
+        d += d >= lo;
+        d += d >= hi;
+        h[r] = hrow[c * K + d];
+      }
+      uint64_t T[2][P2];
+      uint64_t tmax = 0, acc = 0;
+      // stage-1 products stay below 2^63 when every factor entry is < 2^44
+      // (host bound, or a u32 table): counters < 2^16, at most 6 terms
+      const bool safe = A.f_safe != 0 || NARROW || FK == 0;
+#pragma unroll
+      for (int o = 0; o < 2; ++o) {
+        const uint32_t c0 = o ? cb : ca, c1 = o ? ca : cb;
+        // F'[q]: the pivot factor's entry for the q-th (T1-1)-subset of R
+        uint64_t Fp[NB];
+        if (FK == 0) {
+          Fp[0] = 1;
+        } else if (FK == 3) {
+          const uint64_t s = (o == 0) != (A.sw01 != 0) ? sab : sba;
+          const uint64_t* row = A.F + s * A.rsF + c * A.PF;
+#pragma unroll
+          for (int q = 0; q < NB; ++q) Fp[q] = __ldg(row + q);
+        } else {
+          const uint32_t v = FK == 1 ? (o ? b : a) : (o ? a : b);
+          const uint32_t cf = FK == 1 ? c0 : c1, cx = FK == 1 ? c1 : c0;
+          const uint8_t* mp = fmap + (cf * K + cx) * NB;
+          const uint64_t ro = static_cast<uint64_t>(v) * A.rsF + c * A.PF;
+#pragma unroll
+          for (int q = 0; q < NB; ++q) {
+            const uint32_t ix = mp[q];
+            Fp[q] = NARROW ? static_cast<uint64_t>(__ldg(reinterpret_cast<const uint32_t*>(A.F) + ro + ix))
+                           : __ldg(A.F + ro + ix);
+          }
+        }
+        // stage 1: T[i] = sum over r in A_i of h[r] * F'[A_i \ r]
+        canon::sfor<P2>([&](auto ii) {
+          constexpr int i = decltype(ii)::value;
+          constexpr uint32_t Ai = canon::nth_subset(M, T1, i);
+          uint64_t v = 0;
+          canon::sfor<T1>([&](auto bb) {
+            constexpr int r = canon::nth_bit(Ai, decltype(bb)::value);
+            constexpr int q = FK ? canon::crank(Ai & ~(1u << r)) : 0;
+            const uint64_t f = Fp[q];
+            if (safe) {
+              v += f * h[r];
+            } else {
+              ovf |= __umul64hi(f, h[r]) != 0;
+              const uint64_t fh = f * h[r];
+              v += fh;
+              ovf |= v < fh;
+            }
+          });
+          T[o][i] = v;
+          tmax |= v;
+          if (!SP) {  // unfused: this block's output
+            updl += v != 0;
+            if (A.out_kind == 2) {
+              A.out[static_cast<uint64_t>(o ? sba : sab) * A.rso + c * A.Pout + i] = v;
+            } else if (A.out_kind == 0) {
+              acc += v;
+              ovf |= acc < v;
+            } else if (v) {
+              atomic_add_ck(reinterpret_cast<u64*>(A.out) + static_cast<uint64_t>(o ? b : a) * A.rso + c * A.Pout +
+                                idx1[(c0 * K + c1) * P2 + i],
+                            v, A.err);
+            }
+          }
+        });
+      }
+      if (SP) {
+        // stage 2: the fused parent on the same edge and histogram; its pivot
+        // factor is this block's row for the orientation it reads
+        const bool safe2 = (tmax >> 44) == 0;
+#pragma unroll
+        for (int o = 0; o < 2; ++o) {
+          const uint32_t c0 = o ? cb : ca, c1 = o ? ca : cb;
+          const int osel = ((o == 0) != (A.sw01p != 0)) ? 0 : 1;
+          canon::sfor<P2p>([&](auto ii) {
+            constexpr int i = decltype(ii)::value;
+            constexpr uint32_t Ai = canon::nth_subset(M, TP, i);
+            uint64_t v = 0;
+            canon::sfor<TP>([&](auto bb) {
+              constexpr int r = canon::nth_bit(Ai, decltype(bb)::value);
+              constexpr int q = canon::crank(Ai & ~(1u << r));
+              const uint64_t f = osel ? T[1][q] : T[0][q];
+              if (safe2) {
+                v += f * h[r];
+              } else {
+                ovf |= __umul64hi(f, h[r]) != 0;
+                const uint64_t fh = f * h[r];
+                v += fh;
+                ovf |= v < fh;
+              }
+            });
+            updl += v != 0;
+            if (A.pout_kind == 2) {
+              A.pout[static_cast<uint64_t>(o ? sba : sab) * A.rsop + c * A.Poutp + i] = v;
+            } else if (A.pout_kind == 0) {
+              acc += v;
+              ovf |= acc < v;
+            } else if (v) {
+              atomic_add_ck(reinterpret_cast<u64*>(A.pout) + static_cast<uint64_t>(o ? b : a) * A.rsop +
+                                c * A.Poutp + idx1p[(c0 * K + c1) * P2p + i],
+                            v, A.err);
+            }
+          });
+        }
+      }
+#pragma unroll
+      for (int cc = 0; cc < kChiStride; ++cc)
+        if (cc == c) {
+          local[cc] += acc;
+          ovf |= local[cc] < acc;
+        }
+    }
+    upd += updl;
+  }
+  const bool scalar_out = (!SP && A.out_kind == 0) || (SP && A.pout_kind == 0);
+  if (scalar_out) {
+#pragma unroll
+    for (int c = 0; c < kChiStride; ++c) {
+      uint64_t v = local[c];
+      for (int o = 16; o > 0; o >>= 1) v = add_ck(v, __shfl_down_sync(0xffffffffu, v, o), A.err);
+      if (lane == 0 && v) atomic_add_ck(A.scalars + c, v, A.err);
+    }
+  }
+  if (ovf) atomicOr(A.err, 1);
+  for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(0xffffffffu, upd, o);
+  if (lane == 0 && upd) atomicAdd(A.updates, static_cast<u64>(upd));
+}
+
+// Shared-memory bytes of a tri_canon_kernel launch (the kernel's carve-up).
+inline size_t tri_canon_smem(int K, int S1, int FK, int SP, int out_kind, int pout_kind) {
+  auto bn = [](int n, int r) { return canon::cbinom(n, r); };
+  const int M = K - 2, NB = FK ? bn(M, S1 - 3) : 1, P2 = bn(M, S1 - 2), P2p = SP ? bn(M, SP - 2) : 0;
+  const int FMAP = (FK == 1 || FK == 2) ? K * K * NB : 0;
+  const int n1 = out_kind == 1 ? K * K * P2 : 0, n1p = (SP && pout_kind == 1) ? K * K * P2p : 0;
+  const size_t LS = 2 * ((((kChiStride * K) + 1) / 2) | 1);
+  return static_cast<size_t>((FMAP + 3) / 4) * 4 + 2 * static_cast<size_t>(n1 + n1p + ((n1 + n1p) & 1)) +
+         static_cast<size_t>(32 * kHistWarps) * LS * 2;
+}
+
+using TriCanonFn = void (*)(TriHistArgs);
+
+// The instantiated shapes (K, S1, FK, SP, NARROW); others use tri_hist_kernel.
+inline TriCanonFn tri_canon_find(int K, int S1, int FK, int SP, bool narrow) {
+#define MB_CANON(k_, s_, f_, p_, n_) \
+  if (K == k_ && S1 == s_ && FK == f_ && SP == p_ && narrow == n_) return tri_canon_kernel<k_, s_, f_, p_, n_>;
+#define MB_CANON_K(k_)                                                                                    \
+  MB_CANON(k_, 3, 0, 0, false) MB_CANON(k_, 3, 0, 4, false)                                               \
+  MB_CANON(k_, 4, 1, 0, false) MB_CANON(k_, 4, 1, 0, true) MB_CANON(k_, 4, 2, 0, false)                   \
+  MB_CANON(k_, 4, 2, 0, true) MB_CANON(k_, 4, 3, 0, false)                                                \
+  MB_CANON(k_, 5, 1, 6, false) MB_CANON(k_, 5, 1, 6, true) MB_CANON(k_, 5, 2, 6, false)                   \
+  MB_CANON(k_, 5, 2, 6, true)
+  MB_CANON_K(6)
+#undef MB_CANON_K
+#undef MB_CANON
+  return nullptr;
+}
