@@ -27,11 +27,23 @@ struct LeafMapArgs {
   uint32_t rsb, rsa, rso;  // row strides (C_alloc * P)
   int sb, sa, sZ, k, C;
   int unchecked;  // entries provably < 2^62 (host bound): plain adds
-  int ub_n, ua_n, out_n;  // narrow (u32) tables, see bind()
+  int ub_e, ua_e, out_e;  // entry bytes of the tables: 8, or narrow 4 (u32) / 2 (u16), see bind()
   uint64_t* out;
   int* err;
   u64* updates;
 };
+
+// entry idx of a table stored with `e` bytes per entry (8, 4 or 2)
+__device__ __forceinline__ uint64_t ld_entry(const uint64_t* t, uint64_t idx, int e) {
+  if (e == 2) return __ldg(reinterpret_cast<const uint16_t*>(t) + idx);
+  if (e == 4) return __ldg(reinterpret_cast<const uint32_t*>(t) + idx);
+  return __ldg(t + idx);
+}
+__device__ __forceinline__ void st_entry(uint64_t* t, uint64_t idx, int e, uint64_t v) {
+  if (e == 2) reinterpret_cast<uint16_t*>(t)[idx] = static_cast<uint16_t>(v);
+  else if (e == 4) reinterpret_cast<uint32_t*>(t)[idx] = static_cast<uint32_t>(v);
+  else t[idx] = v;
+}
 
 __device__ __forceinline__ uint32_t leaf_map_size(const LeafMapArgs& A) {
   return static_cast<uint32_t>(A.k) * A.k * (A.ub ? A.Pb : 1u);
@@ -87,7 +99,53 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
     // one lane per (neighbour, colouring): low-degree rows still fill the
     // warp, and a neighbour's C rows are read as one contiguous span
     const uint32_t items = deg * static_cast<uint32_t>(A.C);
-    for (uint32_t it = lane; it < items; it += GROUP) {
+    if (PB > 0 && PB <= 8 && A.ub && A.ub_e != 8 && (k32 || A.unchecked)) {
+      // constant child row: two items per lane in flight (their neighbour
+      // ids, colours and rows are all loaded before either is consumed)
+      constexpr int PBc = PB > 0 && PB <= 8 ? PB : 1;
+      for (uint32_t it0 = lane; it0 < items; it0 += 2 * GROUP) {
+        uint32_t y[2], cy[2];
+        int cc[2];
+        bool ok[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const uint32_t it = it0 + u * GROUP;
+          ok[u] = it < items;
+          const uint32_t j = cpow2 ? it >> clog : it / static_cast<uint32_t>(A.C);
+          cc[u] = static_cast<int>(it - j * static_cast<uint32_t>(A.C));
+          y[u] = ok[u] ? __ldg(A.adj + base + j) : 0u;
+        }
+        uint32_t r[2][PBc];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          cy[u] = ok[u] ? A.chi[static_cast<uint64_t>(y[u]) * kChiStride + cc[u]] : 0xFFu;
+          const uint64_t roff = static_cast<uint64_t>(y[u]) * A.rsb + cc[u] * PBc;
+          if (A.ub_e == 2) {
+#pragma unroll
+            for (int e = 0; e < PBc; ++e) r[u][e] = ok[u] ? ld_entry(A.ub, roff + e, 2) : 0u;
+          } else {
+#pragma unroll
+            for (int e = 0; e < PBc; ++e) r[u][e] = ok[u] ? ld_entry(A.ub, roff + e, 4) : 0u;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (!ok[u]) continue;
+          const uint32_t cx = color_of(cxs, cc[u]);
+          if (cy[u] == cx) continue;
+          const uint16_t* my = map + (cx * A.k + cy[u]) * PBc;
+          Acc* Zc = Zw + cc[u] * A.PZ;
+#pragma unroll
+          for (int e = 0; e < PBc; ++e) {
+            if (!r[u][e]) continue;
+            const uint16_t t = my[e];
+            if (t == 0xFFFF) continue;
+            atomicAdd(Zc + t, static_cast<Acc>(r[u][e]));
+            ++upd;
+          }
+        }
+      }
+    } else for (uint32_t it = lane; it < items; it += GROUP) {
       const uint32_t j = cpow2 ? it >> clog : it / static_cast<uint32_t>(A.C);
       const int c = static_cast<int>(it - j * static_cast<uint32_t>(A.C));
       const uint32_t y = __ldg(A.adj + base + j);
@@ -104,17 +162,18 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
       }
       if (cy == cx) continue;
       const uint64_t roff = static_cast<uint64_t>(y) * A.rsb + c * pb;
-      const uint64_t* row = A.ub + roff;
-      const uint32_t* row32 = reinterpret_cast<const uint32_t*>(A.ub) + roff;
       for (uint32_t i0 = 0; i0 < pb; i0 += 8) {
         // the row's loads are issued together, then consumed
         uint64_t r[8];
-        if (A.ub_n) {
+        if (A.ub_e == 2) {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) r[u] = i0 + u < pb ? __ldg(row32 + i0 + u) : 0u;
+          for (int u = 0; u < 8; ++u) r[u] = i0 + u < pb ? ld_entry(A.ub, roff + i0 + u, 2) : 0u;
+        } else if (A.ub_e == 4) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) r[u] = i0 + u < pb ? ld_entry(A.ub, roff + i0 + u, 4) : 0u;
         } else {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) r[u] = i0 + u < pb ? __ldg(row + i0 + u) : 0ull;
+          for (int u = 0; u < 8; ++u) r[u] = i0 + u < pb ? ld_entry(A.ub, roff + i0 + u, 8) : 0ull;
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -139,13 +198,9 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
       }
       __syncthreads();
     }
-    uint64_t* orow = A.out + static_cast<uint64_t>(x) * A.rso;
     if (!A.ua) {
-      if (A.out_n)
-        for (uint32_t i = lane; i < A.C * A.Pout; i += GROUP)
-          reinterpret_cast<uint32_t*>(A.out)[static_cast<uint64_t>(x) * A.rso + i] = static_cast<uint32_t>(Z[i]);
-      else
-        for (uint32_t i = lane; i < A.C * A.Pout; i += GROUP) orow[i] = static_cast<uint64_t>(Z[i]);
+      for (uint32_t i = lane; i < A.C * A.Pout; i += GROUP)
+        st_entry(A.out, static_cast<uint64_t>(x) * A.rso + i, A.out_e, static_cast<uint64_t>(Z[i]));
     } else {
       const uint64_t per = static_cast<uint64_t>(A.PZ) * A.Pa;
       for (uint64_t it = lane; it < per * A.C; it += GROUP) {
@@ -155,7 +210,7 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
         const uint64_t z = Z[c * A.PZ + iz];
         if (!z) continue;
         const uint64_t aoff = static_cast<uint64_t>(x) * A.rsa + c * A.Pa + ia;
-        const uint64_t a = A.ua_n ? __ldg(reinterpret_cast<const uint32_t*>(A.ua) + aoff) : __ldg(A.ua + aoff);
+        const uint64_t a = ld_entry(A.ua, aoff, A.ua_e);
         if (!a) continue;
         const uint32_t fx = 1u << color_of(cxs, c);
         const uint32_t Mz = sig_expand(sig_unrank(c_lut, A.sZ - 1, iz), fx);
@@ -167,11 +222,8 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
         ++upd;
       }
       if (GROUP == 32) __syncwarp(); else __syncthreads();
-      if (A.out_n)
-        for (uint32_t i = lane; i < A.C * A.Pout; i += GROUP)
-          reinterpret_cast<uint32_t*>(A.out)[static_cast<uint64_t>(x) * A.rso + i] = static_cast<uint32_t>(O[i]);
-      else
-        for (uint32_t i = lane; i < A.C * A.Pout; i += GROUP) orow[i] = static_cast<uint64_t>(O[i]);
+      for (uint32_t i = lane; i < A.C * A.Pout; i += GROUP)
+        st_entry(A.out, static_cast<uint64_t>(x) * A.rso + i, A.out_e, static_cast<uint64_t>(O[i]));
     }
     if (GROUP == 32) __syncwarp(); else __syncthreads();
   }
@@ -235,7 +287,6 @@ __global__ void __launch_bounds__(256) leaf_hist_kernel(LeafMapArgs A, const uin
     }
     flush();
     const uint64_t cxs = load_colors(A.chi, x);
-    uint64_t* orow = A.out + static_cast<uint64_t>(x) * A.rso;
 #pragma unroll
     for (int c = 0; c < kChiStride; ++c) {
       if (c >= A.C) break;
@@ -245,12 +296,87 @@ __global__ void __launch_bounds__(256) leaf_hist_kernel(LeafMapArgs A, const uin
         if (d >= A.k || d == static_cast<int>(cx)) continue;
         const uint32_t v = (H[c][d >> 1] >> (16 * (d & 1))) & 0xFFFFu;
         const uint32_t col = c * A.Pout + d - (d > static_cast<int>(cx) ? 1 : 0);
-        if (A.out_n) reinterpret_cast<uint32_t*>(A.out)[static_cast<uint64_t>(x) * A.rso + col] = v;
-        else orow[col] = v;
+        st_entry(A.out, static_cast<uint64_t>(x) * A.rso + col, A.out_e, v);
         upd += v != 0;
       }
     }
   }
   for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(0xffffffffu, upd, o);
   if ((threadIdx.x & 31) == 0 && upd) atomicAdd(A.updates, static_cast<u64>(upd));
+}
+
+// First leaf level for heavy vertices (degree > 256): a CTA per vertex, each
+// thread counts a strided slice of the row in registers as leaf_hist_kernel
+// does, then the CTA sums the packed 16-bit counters (warp shuffles, then
+// across warps in shared memory).  Counts stay below 2^16 (the host checks
+// maxdeg < 65536).  Replaces one shared-memory atomic per (neighbour,
+// colouring) on a few hot counters.
+__global__ void __launch_bounds__(256) leaf_hist_heavy_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist,
+                                                              uint32_t nv) {
+  __shared__ uint32_t red[8][kChiStride * 4];
+  uint64_t upd = 0;
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (uint32_t gi = blockIdx.x; gi < nv; gi += gridDim.x) {
+    const uint32_t x = vlist[gi];
+    uint32_t N[kChiStride], H[kChiStride][4];
+#pragma unroll
+    for (int c = 0; c < kChiStride; ++c) {
+      N[c] = 0;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) H[c][w] = 0;
+    }
+    auto flush = [&]() {
+#pragma unroll
+      for (int c = 0; c < kChiStride; ++c) {
+        const uint32_t ev = N[c] & 0x0F0F0F0Fu, od = (N[c] >> 4) & 0x0F0F0F0Fu;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) H[c][w] += ((ev >> (8 * w)) & 0xFFu) | (((od >> (8 * w)) & 0xFFu) << 16);
+        N[c] = 0;
+      }
+    };
+    const uint64_t base = A.off[x], end = A.off[x + 1];
+    int pend = 0;
+    for (uint64_t p = base + threadIdx.x; p < end; p += 256) {
+      const uint64_t cw = load_colors(A.chi, __ldg(A.adj + p));
+      const uint32_t lo32 = static_cast<uint32_t>(cw), hi32 = static_cast<uint32_t>(cw >> 32);
+#pragma unroll
+      for (int c = 0; c < kChiStride; ++c) {
+        const uint32_t half = c < 4 ? lo32 : hi32;
+        N[c] += 1u << (((half >> (8 * (c & 3))) & 7u) << 2);
+      }
+      if (++pend == 15) {
+        flush();
+        pend = 0;
+      }
+    }
+    flush();
+#pragma unroll
+    for (int c = 0; c < kChiStride; ++c)
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        uint32_t v = H[c][w];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) red[wid][c * 4 + w] = v;
+      }
+    __syncthreads();
+    if (threadIdx.x < kChiStride * 8) {
+      const int c = threadIdx.x >> 3, d = threadIdx.x & 7;
+      if (c < A.C && d < A.k) {
+        const uint32_t cx = color_of(load_colors(A.chi, x), c);
+        if (d != static_cast<int>(cx)) {
+          uint32_t v = 0;
+#pragma unroll
+          for (int w = 0; w < 8; ++w) v += red[w][c * 4 + (d >> 1)];
+          v = (v >> (16 * (d & 1))) & 0xFFFFu;
+          st_entry(A.out, static_cast<uint64_t>(x) * A.rso + c * A.Pout + d - (d > static_cast<int>(cx) ? 1 : 0),
+                   A.out_e, v);
+          upd += v != 0;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(0xffffffffu, upd, o);
+  if (lane == 0 && upd) atomicAdd(A.updates, static_cast<u64>(upd));
 }
