@@ -380,3 +380,81 @@ __global__ void __launch_bounds__(256) leaf_hist_heavy_kernel(LeafMapArgs A, con
   for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(0xffffffffu, upd, o);
   if (lane == 0 && upd) atomicAdd(A.updates, static_cast<u64>(upd));
 }
+
+// Leaf block with a child row on the leaf side and no annotation on the
+// boundary (U_out[x] = sum over neighbours y of U_b[y] shifted by chi(x)),
+// light vertices: a thread per (vertex, colouring slot) — 8 consecutive lanes
+// share a vertex, a warp covers 4 vertices of similar degree.  Each thread
+// walks its vertex's row and adds the child entries into private accumulators
+// (shared memory, odd stride: no atomics, no bank conflicts), then writes its
+// output row; the 8 rows of a vertex are one contiguous span.  Two neighbours
+// are in flight per thread.  Requires entries < 2^32 (host bound) and a narrow
+// child table.
+template <int PB>
+__global__ void __launch_bounds__(256) leaf_pull_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist,
+                                                        uint32_t nv) {
+  extern __shared__ u64 lsm[];
+  const uint32_t msize = leaf_map_size(A);
+  uint16_t* map = reinterpret_cast<uint16_t*>(lsm);
+  uint32_t* accs = reinterpret_cast<uint32_t*>(lsm + (msize * 2 + 7) / 8);
+  for (uint32_t i = threadIdx.x; i < msize; i += blockDim.x) {
+    const uint32_t ib = i % PB, cy = (i / PB) % A.k, cx = i / (PB * A.k);
+    uint16_t t = 0xFFFF;
+    if (cx != cy) {
+      const uint32_t fx = 1u << cx, fy = 1u << cy;
+      const uint32_t Mb = sig_expand(sig_unrank(c_lut, A.sb - 1, ib), fy);
+      if (!(Mb & fx)) t = static_cast<uint16_t>(sig_index(c_lut, Mb | fx, fx));
+    }
+    map[i] = t;
+  }
+  __syncthreads();
+  const uint32_t AS = A.Pout | 1u;
+  uint32_t* acc = accs + threadIdx.x * AS;
+  const int c = threadIdx.x & 7;
+  uint32_t upd = 0;
+  for (uint32_t gi = blockIdx.x * 32 + (threadIdx.x >> 3); gi < nv; gi += gridDim.x * 32) {
+    if (c >= A.C) continue;
+    const uint32_t x = vlist[gi];
+    for (uint32_t i = 0; i < A.Pout; ++i) acc[i] = 0;
+    const uint32_t cx = A.chi[static_cast<uint64_t>(x) * kChiStride + c];
+    const uint16_t* mx = map + cx * A.k * PB;
+    const uint64_t base = A.off[x], end = A.off[x + 1];
+    for (uint64_t p = base; p < end; p += 2) {
+      uint32_t y[2], cy[2], r[2][PB];
+      bool ok[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        ok[u] = p + u < end;
+        y[u] = ok[u] ? __ldg(A.adj + p + u) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        cy[u] = ok[u] ? A.chi[static_cast<uint64_t>(y[u]) * kChiStride + c] : cx;
+        const uint64_t roff = static_cast<uint64_t>(y[u]) * A.rsb + c * PB;
+        if (A.ub_e == 2) {
+#pragma unroll
+          for (int e = 0; e < PB; ++e) r[u][e] = ok[u] ? ld_entry(A.ub, roff + e, 2) : 0u;
+        } else {
+#pragma unroll
+          for (int e = 0; e < PB; ++e) r[u][e] = ok[u] ? ld_entry(A.ub, roff + e, 4) : 0u;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (cy[u] == cx) continue;
+        const uint16_t* my = mx + cy[u] * PB;
+#pragma unroll
+        for (int e = 0; e < PB; ++e) {
+          const uint16_t t = my[e];
+          if (t == 0xFFFF || !r[u][e]) continue;
+          acc[t] += r[u][e];
+          ++upd;
+        }
+      }
+    }
+    for (uint32_t i = 0; i < A.Pout; ++i)
+      st_entry(A.out, static_cast<uint64_t>(x) * A.rso + c * A.Pout + i, A.out_e, acc[i]);
+  }
+  for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(0xffffffffu, upd, o);
+  if ((threadIdx.x & 31) == 0 && upd) atomicAdd(A.updates, static_cast<u64>(upd));
+}
