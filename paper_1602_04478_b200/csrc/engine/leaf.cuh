@@ -458,3 +458,82 @@ __global__ void __launch_bounds__(256) leaf_pull_kernel(LeafMapArgs A, const uin
   for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(0xffffffffu, upd, o);
   if ((threadIdx.x & 31) == 0 && upd) atomicAdd(A.updates, static_cast<u64>(upd));
 }
+
+// Heavy-vertex counterpart of leaf_pull_kernel: a CTA per vertex, thread t
+// owns colouring slot t & 7 and every 32nd neighbour from t >> 3 (the 8 rows
+// of a neighbour are read by 8 consecutive lanes), private accumulators, then
+// the 32 partial rows of each colouring are summed in shared memory.
+template <int PB>
+__global__ void __launch_bounds__(256) leaf_pull_heavy_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist,
+                                                              uint32_t nv) {
+  extern __shared__ u64 lsm[];
+  const uint32_t msize = leaf_map_size(A);
+  uint16_t* map = reinterpret_cast<uint16_t*>(lsm);
+  uint32_t* accs = reinterpret_cast<uint32_t*>(lsm + (msize * 2 + 7) / 8);
+  for (uint32_t i = threadIdx.x; i < msize; i += blockDim.x) {
+    const uint32_t ib = i % PB, cy = (i / PB) % A.k, cx = i / (PB * A.k);
+    uint16_t t = 0xFFFF;
+    if (cx != cy) {
+      const uint32_t fx = 1u << cx, fy = 1u << cy;
+      const uint32_t Mb = sig_expand(sig_unrank(c_lut, A.sb - 1, ib), fy);
+      if (!(Mb & fx)) t = static_cast<uint16_t>(sig_index(c_lut, Mb | fx, fx));
+    }
+    map[i] = t;
+  }
+  const uint32_t AS = A.Pout | 1u;
+  uint32_t* acc = accs + threadIdx.x * AS;
+  const int c = threadIdx.x & 7, jl = threadIdx.x >> 3;
+  uint32_t upd = 0;
+  for (uint32_t gi = blockIdx.x; gi < nv; gi += gridDim.x) {
+    const uint32_t x = vlist[gi];
+    __syncthreads();  // map ready (first vertex) / previous vertex's sums read
+    for (uint32_t i = 0; i < A.Pout; ++i) acc[i] = 0;
+    if (c < A.C) {
+      const uint32_t cx = A.chi[static_cast<uint64_t>(x) * kChiStride + c];
+      const uint16_t* mx = map + cx * A.k * PB;
+      const uint64_t base = A.off[x], end = A.off[x + 1];
+      for (uint64_t p = base + jl; p < end; p += 64) {
+        uint32_t y[2], cy[2], r[2][PB];
+        bool ok[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          ok[u] = p + 32 * u < end;
+          y[u] = ok[u] ? __ldg(A.adj + p + 32 * u) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          cy[u] = ok[u] ? A.chi[static_cast<uint64_t>(y[u]) * kChiStride + c] : cx;
+          const uint64_t roff = static_cast<uint64_t>(y[u]) * A.rsb + c * PB;
+          if (A.ub_e == 2) {
+#pragma unroll
+            for (int e = 0; e < PB; ++e) r[u][e] = ok[u] ? ld_entry(A.ub, roff + e, 2) : 0u;
+          } else {
+#pragma unroll
+            for (int e = 0; e < PB; ++e) r[u][e] = ok[u] ? ld_entry(A.ub, roff + e, 4) : 0u;
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          if (cy[u] == cx) continue;
+          const uint16_t* my = mx + cy[u] * PB;
+#pragma unroll
+          for (int e = 0; e < PB; ++e) {
+            const uint16_t t = my[e];
+            if (t == 0xFFFF || !r[u][e]) continue;
+            acc[t] += r[u][e];
+            ++upd;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    for (uint32_t o = threadIdx.x; o < A.C * A.Pout; o += blockDim.x) {
+      const uint32_t cc = o / A.Pout, i = o - cc * A.Pout;
+      uint32_t s = 0;
+      for (int l = 0; l < 32; ++l) s += accs[(l * 8 + cc) * AS + i];
+      st_entry(A.out, static_cast<uint64_t>(x) * A.rso + o, A.out_e, s);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(0xffffffffu, upd, o);
+  if ((threadIdx.x & 31) == 0 && upd) atomicAdd(A.updates, static_cast<u64>(upd));
+}
