@@ -243,9 +243,12 @@ __global__ void k_reverse_slots(uint64_t m2, const uint64_t* __restrict__ off,
 
 // Colourings c0..c0+C-1 (row-major [colouring][vertex], colours 1..k) into the
 // interleaved 0-based layout [vertex][kChiStride]; unused slots are zeroed.
+// out4 (optional) gets the same colours times 4 (the nibble offset the 3-cycle
+// histograms shift by).
 __global__ void k_recolor(uint32_t n, int C, const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int k,
-                          int* err, const uint32_t* __restrict__ order) {
+                          int* err, const uint32_t* __restrict__ order, uint64_t* __restrict__ out4) {
   const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v == n && out4) out4[n] = 0x1C1C1C1C1C1C1C1Cull;  // dummy vertex: colour 7 in every slot
   if (v >= n) return;
   const uint32_t src = order[v];  // caller's id of device vertex v
   unsigned long long cols = 0;
@@ -258,6 +261,7 @@ __global__ void k_recolor(uint32_t n, int C, const uint8_t* __restrict__ in, uin
     }
   }
   reinterpret_cast<unsigned long long*>(out)[v] = cols;
+  if (out4) out4[v] = cols << 2;
 }
 
 // The kChiStride colours of vertex v (one 8-byte load) and colour slot c of them.

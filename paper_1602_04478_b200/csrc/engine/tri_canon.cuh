@@ -125,6 +125,144 @@ __device__ __forceinline__ void lane_histogram(const TriHistArgs& A, uint64_t j,
   flush();
 }
 
+// lane_histogram with the 16-byte list loads one chunk ahead (the next chunk is
+// in flight while the current one's colours are gathered and counted) and
+// colours pre-scaled by 4 (chi4): a colouring's count is one funnel shift and
+// one add.  For K < 8 entries past the list end count into the unused colour
+// 7 instead of being tested.
+template <int K>
+__device__ __forceinline__ void lane_histogram4(const TriHistArgs& A, uint64_t j, uint32_t (&H)[kChiStride][4]) {
+  uint32_t N[kChiStride];
+#pragma unroll
+  for (int c = 0; c < kChiStride; ++c) {
+    N[c] = 0;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) H[c][w] = 0;
+  }
+  auto flush = [&]() {
+#pragma unroll
+    for (int c = 0; c < kChiStride; ++c) {
+      const uint32_t ev = N[c] & 0x0F0F0F0Fu, od = (N[c] >> 4) & 0x0F0F0F0Fu;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) H[c][w] += ((ev >> (8 * w)) & 0xFFu) | (((od >> (8 * w)) & 0xFFu) << 16);
+      N[c] = 0;
+    }
+  };
+  constexpr uint64_t kDummy = 0x1C1C1C1C1C1C1C1Cull;  // colour 7 (times 4) in every slot
+  const uint64_t lo_ = A.cn_off[j], hi_ = A.cn_off[j + 1];
+  uint64_t p = lo_ & ~3ull;
+  uint4 q = p < hi_ ? __ldg(reinterpret_cast<const uint4*>(A.cn_w + p)) : make_uint4(0, 0, 0, 0);
+  int pend = 0;
+  for (; p < hi_; p += 4) {
+    const uint4 qn = p + 4 < hi_ ? __ldg(reinterpret_cast<const uint4*>(A.cn_w + p + 4)) : q;
+    const uint32_t ws[4] = {q.x, q.y, q.z, q.w};
+    uint64_t cw[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const bool in = p + u >= lo_ && p + u < hi_;
+      cw[u] = in ? __ldg(A.chi4 + ws[u]) : (K < 8 ? kDummy : ~0ull);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (K == 8 && cw[u] == ~0ull) continue;
+      const uint32_t lo32 = static_cast<uint32_t>(cw[u]), hi32 = static_cast<uint32_t>(cw[u] >> 32);
+#pragma unroll
+      for (int c = 0; c < kChiStride; ++c) {
+        const uint32_t half = c < 4 ? lo32 : hi32;
+        // 1 << (4 * colour): the shift uses the low 5 bits, the byte holds 4 * colour < 32
+        N[c] += __funnelshift_l(0u, 1u, half >> (8 * (c & 3)));
+      }
+    }
+    if (++pend == 3) {
+      flush();
+      pend = 0;
+    }
+    q = qn;
+  }
+  flush();
+}
+
+// The lane's histogram row for oriented edge j, written to hrow[c*K + d]
+// (u16: lane-mode lists are shorter than 65536).  Three counter levels keep
+// the per-entry work to one funnel shift and one add per colouring:
+//   N[c]  4-bit fields, all colours of colouring slot c in one word (an entry
+//         adds 1 << (4 * colour); chi4 holds the colours pre-scaled by 4 and
+//         the shift uses the low 5 bits of the byte), moved every 12 entries
+//         into
+//   B[c]  8-bit fields (even / odd colours), moved every 240 entries into
+//   hrow  the 16-bit row in shared memory (read-modify-write, rare).
+// The list is read with 16-byte loads, the next chunk in flight while the
+// current one is counted.  For K < 8 slots outside the list count vertex
+// A.nv, whose chi4 word is colour 7 (unused) in every slot, so the inner loop
+// has no branches; for K = 8 they are skipped.
+template <int K>
+__device__ __forceinline__ void lane_histogram_row(const TriHistArgs& A, uint64_t j, uint16_t* hrow) {
+  uint32_t N[kChiStride], Be[kChiStride], Bo[kChiStride];
+#pragma unroll
+  for (int c = 0; c < kChiStride; ++c) N[c] = Be[c] = Bo[c] = 0;
+  bool spilled = false;
+  auto flushN = [&]() {
+#pragma unroll
+    for (int c = 0; c < kChiStride; ++c) {
+      Be[c] += N[c] & 0x0F0F0F0Fu;
+      Bo[c] += (N[c] >> 4) & 0x0F0F0F0Fu;
+      N[c] = 0;
+    }
+  };
+  auto flushB = [&]() {
+#pragma unroll
+    for (int c = 0; c < kChiStride; ++c) {
+#pragma unroll
+      for (int d = 0; d < K; ++d) {
+        const uint32_t v = (((d & 1) ? Bo[c] : Be[c]) >> (8 * (d >> 1))) & 0xFFu;
+        hrow[c * K + d] = static_cast<uint16_t>(spilled ? hrow[c * K + d] + v : v);
+      }
+      Be[c] = Bo[c] = 0;
+    }
+    spilled = true;
+  };
+  const uint64_t lo = A.cn_off[j], hi = A.cn_off[j + 1];
+  const uint64_t p0 = lo & ~3ull;
+  const uint32_t head = static_cast<uint32_t>(lo - p0), n = static_cast<uint32_t>(hi - p0);
+  const uint32_t nch = (n + 3) >> 2;
+  const uint4* src = reinterpret_cast<const uint4*>(A.cn_w + p0);
+  uint4 q = nch ? __ldg(src) : make_uint4(0, 0, 0, 0);
+  int pend = 0, nfl = 0;
+  for (uint32_t ch = 0; ch < nch; ++ch) {
+    const uint4 qn = ch + 1 < nch ? __ldg(src + ch + 1) : q;
+    const uint32_t ws[4] = {q.x, q.y, q.z, q.w};
+    uint64_t cw[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t idx = 4 * ch + u;
+      const bool in = idx >= head && idx < n;
+      if (K < 8) cw[u] = __ldg(A.chi4 + (in ? ws[u] : A.nv));
+      else cw[u] = in ? __ldg(A.chi4 + ws[u]) : ~0ull;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (K == 8 && cw[u] == ~0ull) continue;
+      const uint32_t lo32 = static_cast<uint32_t>(cw[u]), hi32 = static_cast<uint32_t>(cw[u] >> 32);
+#pragma unroll
+      for (int c = 0; c < kChiStride; ++c) {
+        const uint32_t half = c < 4 ? lo32 : hi32;
+        N[c] += __funnelshift_l(0u, 1u, half >> (8 * (c & 3)));
+      }
+    }
+    if (++pend == 3) {
+      flushN();
+      pend = 0;
+      if (++nfl == 20) {
+        flushB();
+        nfl = 0;
+      }
+    }
+    q = qn;
+  }
+  flushN();
+  flushB();
+}
+
 __device__ __forceinline__ void prefetch_l2(const void* p) {
   asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
@@ -209,16 +347,49 @@ __global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_canon_kernel
       prefetch_span(F + static_cast<uint64_t>(sab) * A.rsF * 8u, fbytes);
       prefetch_span(F + static_cast<uint64_t>(sba) * A.rsF * 8u, fbytes);
     }
-    uint32_t H[kChiStride][4];
-    lane_histogram(A, j, H);
-#pragma unroll
-    for (int c = 0; c < kChiStride; ++c)
-#pragma unroll
-      for (int d = 0; d < 8; ++d)  // static indices keep H in registers
-        if (d < K) hrow[c * K + d] = static_cast<uint16_t>(H[c][d >> 1] >> (16 * (d & 1)));
+    if (!(A.debug & 2)) lane_histogram_row<K>(A, j, hrow);
+    if (A.debug & 1) continue;
     const uint64_t cas = load_colors(A.chi, a), cbs = load_colors(A.chi, b);
     uint32_t updl = 0;
-    for (int c = 0; c < C; ++c) {
+    using FT = typename std::conditional<NARROW, uint32_t, uint64_t>::type;
+    // F'[o][q]: the pivot factor's entry for the q-th (T1-1)-subset of R in
+    // orientation o; loaded one colouring ahead of its use
+    auto load_f = [&](int c, FT (&Fo)[2][NB]) {
+      const uint32_t ca = color_of(cas, c), cb = color_of(cbs, c);
+#pragma unroll
+      for (int o = 0; o < 2; ++o) {
+        const uint32_t c0 = o ? cb : ca, c1 = o ? ca : cb;
+        if (FK == 0) {
+          Fo[o][0] = 1;
+        } else if (ca == cb) {
+#pragma unroll
+          for (int q = 0; q < NB; ++q) Fo[o][q] = 0;
+        } else if (FK == 3) {
+          const uint64_t s = (o == 0) != (A.sw01 != 0) ? sab : sba;
+          const uint64_t* row = A.F + s * A.rsF + c * A.PF;
+#pragma unroll
+          for (int q = 0; q < NB; ++q) Fo[o][q] = static_cast<FT>(__ldg(row + q));
+        } else {
+          const uint32_t v = FK == 1 ? (o ? b : a) : (o ? a : b);
+          const uint32_t cf = FK == 1 ? c0 : c1, cx = FK == 1 ? c1 : c0;
+          const uint8_t* mp = fmap + (cf * K + cx) * NB;
+          const uint64_t ro = static_cast<uint64_t>(v) * A.rsF + c * A.PF;
+#pragma unroll
+          for (int q = 0; q < NB; ++q) {
+            const uint32_t ix = mp[q];
+            if (NARROW) Fo[o][q] = static_cast<FT>(__ldg(reinterpret_cast<const uint32_t*>(A.F) + ro + ix));
+            else Fo[o][q] = static_cast<FT>(__ldg(A.F + ro + ix));
+          }
+        }
+      }
+    };
+    FT Fc[2][NB];
+    load_f(0, Fc);
+#pragma unroll
+    for (int c = 0; c < kChiStride; ++c) {
+      if (c >= C) break;
+      FT Fn[2][NB];
+      if (c + 1 < C) load_f(c + 1, Fn);  // in flight while colouring c is joined
       const uint32_t ca = color_of(cas, c), cb = color_of(cbs, c);
       if (ca == cb) {
         // no colourful match on this edge: materialised edge rows are zero
@@ -229,8 +400,7 @@ __global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_canon_kernel
           for (int o = 0; o < 2; ++o)
             for (uint32_t i = 0; i < A.Poutp; ++i)
               A.pout[static_cast<uint64_t>(o ? sba : sab) * A.rsop + c * A.Poutp + i] = 0;
-        continue;
-      }
+      } else {
       const uint32_t lo = min(ca, cb), hi = max(ca, cb);
       // h[r] = count of the r-th colour not in {ca, cb}
       uint32_t h[M];
@@ -241,35 +411,68 @@ __global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_canon_kernel
         d += d >= hi;
         h[r] = hrow[c * K + d];
       }
+      uint64_t acc = 0;
+      if (SP && A.t_safe) {
+        // Fused child and parent as one bilinear form in h: with
+        //   T[S] = sum_{r' in S} h[r'] F'[S \ r'],  U[A] = sum_{r in A} h[r] T[A \ r]
+        // U[A] = 2 * sum over pairs {r, r'} in A of h[r] h[r'] F'[A \ {r, r'}].
+        // The pair products (< 2^32) are shared by both orientations; every
+        // term is one 32x32->64 (or 32x64) multiply-add, and the host bound on
+        // the child's entries (< 2^44) keeps U below 2^63.
+        constexpr int NPAIR = M * (M - 1) / 2;
+        uint32_t PP[NPAIR > 0 ? NPAIR : 1];
+        canon::sfor<M>([&](auto r1c) {
+          canon::sfor<M>([&](auto r2c) {
+            constexpr int r1 = decltype(r1c)::value, r2 = decltype(r2c)::value;
+            if constexpr (r1 < r2) PP[canon::crank((1u << r1) | (1u << r2))] = h[r1] * h[r2];
+          });
+        });
+        auto pairs = [&](int o, const FT (&Fs)[NB]) {
+          const uint32_t c0 = o ? cb : ca, c1 = o ? ca : cb;
+          canon::sfor<P2p>([&](auto ii) {
+            constexpr int i = decltype(ii)::value;
+            constexpr uint32_t Ai = canon::nth_subset(M, TP, i);
+            uint64_t v = 0;
+            canon::sfor<M>([&](auto r1c) {
+              canon::sfor<M>([&](auto r2c) {
+                constexpr int r1 = decltype(r1c)::value, r2 = decltype(r2c)::value;
+                if constexpr (r1 < r2 && ((Ai >> r1) & 1u) && ((Ai >> r2) & 1u)) {
+                  constexpr uint32_t pr = (1u << r1) | (1u << r2);
+                  constexpr int q = FK ? canon::crank(Ai & ~pr) : 0;
+                  v += static_cast<uint64_t>(PP[canon::crank(pr)]) * Fs[q];
+                }
+              });
+            });
+            v *= 2;
+            updl += v != 0;
+            if (A.pout_kind == 2) {
+              A.pout[static_cast<uint64_t>(o ? sba : sab) * A.rsop + c * A.Poutp + i] = v;
+            } else if (A.pout_kind == 0) {
+              acc += v;
+              ovf |= acc < v;
+            } else if (v) {
+              atomic_add_ck(reinterpret_cast<u64*>(A.pout) + static_cast<uint64_t>(o ? b : a) * A.rsop +
+                                c * A.Poutp + idx1p[(c0 * K + c1) * P2p + i],
+                            v, A.err);
+            }
+          });
+        };
+        if (A.pout_kind == 0 || !A.sw01p) {
+          pairs(0, Fc[0]);
+          pairs(1, Fc[1]);
+        } else {
+          pairs(0, Fc[1]);
+          pairs(1, Fc[0]);
+        }
+      } else {
       uint64_t T[2][P2];
-      uint64_t tmax = 0, acc = 0;
+      uint64_t tmax = 0;
       // stage-1 products stay below 2^63 when every factor entry is < 2^44
       // (host bound, or a u32 table): counters < 2^16, at most 6 terms
       const bool safe = A.f_safe != 0 || NARROW || FK == 0;
 #pragma unroll
       for (int o = 0; o < 2; ++o) {
         const uint32_t c0 = o ? cb : ca, c1 = o ? ca : cb;
-        // F'[q]: the pivot factor's entry for the q-th (T1-1)-subset of R
-        uint64_t Fp[NB];
-        if (FK == 0) {
-          Fp[0] = 1;
-        } else if (FK == 3) {
-          const uint64_t s = (o == 0) != (A.sw01 != 0) ? sab : sba;
-          const uint64_t* row = A.F + s * A.rsF + c * A.PF;
-#pragma unroll
-          for (int q = 0; q < NB; ++q) Fp[q] = __ldg(row + q);
-        } else {
-          const uint32_t v = FK == 1 ? (o ? b : a) : (o ? a : b);
-          const uint32_t cf = FK == 1 ? c0 : c1, cx = FK == 1 ? c1 : c0;
-          const uint8_t* mp = fmap + (cf * K + cx) * NB;
-          const uint64_t ro = static_cast<uint64_t>(v) * A.rsF + c * A.PF;
-#pragma unroll
-          for (int q = 0; q < NB; ++q) {
-            const uint32_t ix = mp[q];
-            Fp[q] = NARROW ? static_cast<uint64_t>(__ldg(reinterpret_cast<const uint32_t*>(A.F) + ro + ix))
-                           : __ldg(A.F + ro + ix);
-          }
-        }
         // stage 1: T[i] = sum over r in A_i of h[r] * F'[A_i \ r]
         canon::sfor<P2>([&](auto ii) {
           constexpr int i = decltype(ii)::value;
@@ -278,7 +481,7 @@ __global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_canon_kernel
           canon::sfor<T1>([&](auto bb) {
             constexpr int r = canon::nth_bit(Ai, decltype(bb)::value);
             constexpr int q = FK ? canon::crank(Ai & ~(1u << r)) : 0;
-            const uint64_t f = Fp[q];
+            const uint64_t f = Fc[o][q];
             if (safe) {
               v += f * h[r];
             } else {
@@ -307,12 +510,11 @@ __global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_canon_kernel
       }
       if (SP) {
         // stage 2: the fused parent on the same edge and histogram; its pivot
-        // factor is this block's row for the orientation it reads
-        const bool safe2 = (tmax >> 44) == 0;
-#pragma unroll
-        for (int o = 0; o < 2; ++o) {
+        // factor is this block's row for the orientation it reads (a scalar
+        // output sums both orientations, so any pairing gives the same total)
+        const bool safe2 = A.t_safe != 0 || (tmax >> 44) == 0;
+        auto stage2 = [&](int o, const uint64_t (&Ts)[P2]) {
           const uint32_t c0 = o ? cb : ca, c1 = o ? ca : cb;
-          const int osel = ((o == 0) != (A.sw01p != 0)) ? 0 : 1;
           canon::sfor<P2p>([&](auto ii) {
             constexpr int i = decltype(ii)::value;
             constexpr uint32_t Ai = canon::nth_subset(M, TP, i);
@@ -320,7 +522,7 @@ __global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_canon_kernel
             canon::sfor<TP>([&](auto bb) {
               constexpr int r = canon::nth_bit(Ai, decltype(bb)::value);
               constexpr int q = canon::crank(Ai & ~(1u << r));
-              const uint64_t f = osel ? T[1][q] : T[0][q];
+              const uint64_t f = Ts[q];
               if (safe2) {
                 v += f * h[r];
               } else {
@@ -342,14 +544,25 @@ __global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_canon_kernel
                             v, A.err);
             }
           });
+        };
+        if (A.pout_kind == 0 || !A.sw01p) {
+          stage2(0, T[0]);
+          stage2(1, T[1]);
+        } else {
+          stage2(0, T[1]);
+          stage2(1, T[0]);
         }
       }
+      }
+      local[c] += acc;
+      ovf |= local[c] < acc;
+      }
+      if (c + 1 < C) {
 #pragma unroll
-      for (int cc = 0; cc < kChiStride; ++cc)
-        if (cc == c) {
-          local[cc] += acc;
-          ovf |= local[cc] < acc;
-        }
+        for (int o = 0; o < 2; ++o)
+#pragma unroll
+          for (int q = 0; q < NB; ++q) Fc[o][q] = Fn[o][q];
+      }
     }
     upd += updl;
   }
