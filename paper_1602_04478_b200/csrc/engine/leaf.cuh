@@ -386,27 +386,36 @@ __global__ void __launch_bounds__(256) leaf_hist_heavy_kernel(LeafMapArgs A, con
 // light vertices: a thread per (vertex, colouring slot) — 8 consecutive lanes
 // share a vertex, a warp covers 4 vertices of similar degree.  Each thread
 // walks its vertex's row and adds the child entries into private accumulators
-// (shared memory, odd stride: no atomics, no bank conflicts), then writes its
-// output row; the 8 rows of a vertex are one contiguous span.  Two neighbours
-// are in flight per thread.  Requires entries < 2^32 (host bound) and a narrow
-// child table.
-template <int PB>
+// (shared memory, odd stride, uncontended shared atomics), then writes its
+// output row; the 8 rows of a vertex are one contiguous span.  The output
+// slots of a child row for colours (cx, cy) come from one packed map word
+// (5 bits per entry, 31 = the entry holds cx).  UNR neighbours are in flight
+// per thread.  Requires entries < 2^32 (host bound), a narrow child table,
+// PB <= 12 and Pout < 31.
+__device__ __forceinline__ void build_pmap(const LeafMapArgs& A, int PB, uint64_t* pmap) {
+  for (uint32_t i = threadIdx.x; i < static_cast<uint32_t>(A.k * A.k); i += blockDim.x) {
+    const uint32_t cy = i % A.k, cx = i / A.k;
+    uint64_t w = ~0ull;
+    if (cx != cy) {
+      w = 0;
+      for (int ib = 0; ib < PB; ++ib) {
+        const uint32_t fx = 1u << cx, fy = 1u << cy;
+        const uint32_t Mb = sig_expand(sig_unrank(c_lut, A.sb - 1, ib), fy);
+        const uint64_t t = (Mb & fx) ? 31u : sig_index(c_lut, Mb | fx, fx);
+        w |= t << (5 * ib);
+      }
+    }
+    pmap[i] = w;
+  }
+}
+
+template <int PB, int UNR>
 __global__ void __launch_bounds__(256) leaf_pull_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist,
                                                         uint32_t nv) {
   extern __shared__ u64 lsm[];
-  const uint32_t msize = leaf_map_size(A);
-  uint16_t* map = reinterpret_cast<uint16_t*>(lsm);
-  uint32_t* accs = reinterpret_cast<uint32_t*>(lsm + (msize * 2 + 7) / 8);
-  for (uint32_t i = threadIdx.x; i < msize; i += blockDim.x) {
-    const uint32_t ib = i % PB, cy = (i / PB) % A.k, cx = i / (PB * A.k);
-    uint16_t t = 0xFFFF;
-    if (cx != cy) {
-      const uint32_t fx = 1u << cx, fy = 1u << cy;
-      const uint32_t Mb = sig_expand(sig_unrank(c_lut, A.sb - 1, ib), fy);
-      if (!(Mb & fx)) t = static_cast<uint16_t>(sig_index(c_lut, Mb | fx, fx));
-    }
-    map[i] = t;
-  }
+  uint64_t* pmap = reinterpret_cast<uint64_t*>(lsm);
+  uint32_t* accs = reinterpret_cast<uint32_t*>(lsm + A.k * A.k);
+  build_pmap(A, PB, pmap);
   __syncthreads();
   const uint32_t AS = A.Pout | 1u;
   uint32_t* acc = accs + threadIdx.x * AS;
@@ -417,18 +426,18 @@ __global__ void __launch_bounds__(256) leaf_pull_kernel(LeafMapArgs A, const uin
     const uint32_t x = vlist[gi];
     for (uint32_t i = 0; i < A.Pout; ++i) acc[i] = 0;
     const uint32_t cx = A.chi[static_cast<uint64_t>(x) * kChiStride + c];
-    const uint16_t* mx = map + cx * A.k * PB;
+    const uint64_t* mx = pmap + cx * A.k;
     const uint64_t base = A.off[x], end = A.off[x + 1];
-    for (uint64_t p = base; p < end; p += 2) {
-      uint32_t y[2], cy[2], r[2][PB];
-      bool ok[2];
+    for (uint64_t p = base; p < end; p += UNR) {
+      uint32_t y[UNR], cy[UNR], r[UNR][PB];
+      bool ok[UNR];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < UNR; ++u) {
         ok[u] = p + u < end;
         y[u] = ok[u] ? __ldg(A.adj + p + u) : 0u;
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < UNR; ++u) {
         cy[u] = ok[u] ? A.chi[static_cast<uint64_t>(y[u]) * kChiStride + c] : cx;
         const uint64_t roff = static_cast<uint64_t>(y[u]) * A.rsb + c * PB;
         if (A.ub_e == 2) {
@@ -440,14 +449,14 @@ __global__ void __launch_bounds__(256) leaf_pull_kernel(LeafMapArgs A, const uin
         }
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < UNR; ++u) {
         if (cy[u] == cx) continue;
-        const uint16_t* my = mx + cy[u] * PB;
+        const uint64_t w = mx[cy[u]];
 #pragma unroll
         for (int e = 0; e < PB; ++e) {
-          const uint16_t t = my[e];
-          if (t == 0xFFFF || !r[u][e]) continue;
-          acc[t] += r[u][e];
+          const uint32_t t = static_cast<uint32_t>(w >> (5 * e)) & 31u;
+          if (t == 31u || !r[u][e]) continue;
+          atomicAdd(acc + t, r[u][e]);
           ++upd;
         }
       }
