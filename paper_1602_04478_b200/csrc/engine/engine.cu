@@ -243,12 +243,12 @@ __global__ void k_reverse_slots(uint64_t m2, const uint64_t* __restrict__ off,
 
 // Colourings c0..c0+C-1 (row-major [colouring][vertex], colours 1..k) into the
 // interleaved 0-based layout [vertex][kChiStride]; unused slots are zeroed.
-// out4 (optional) gets the same colours times 4 (the nibble offset the 3-cycle
-// histograms shift by).
+// Row n is the dummy vertex the histogram kernels count for list slots past
+// a row's end: colour 7 (never a real colour when k < 8) in every slot.
 __global__ void k_recolor(uint32_t n, int C, const uint8_t* __restrict__ in, uint8_t* __restrict__ out, int k,
-                          int* err, const uint32_t* __restrict__ order, uint64_t* __restrict__ out4) {
+                          int* err, const uint32_t* __restrict__ order) {
   const uint32_t v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v == n && out4) out4[n] = 0x1C1C1C1C1C1C1C1Cull;  // dummy vertex: colour 7 in every slot
+  if (v == n) reinterpret_cast<unsigned long long*>(out)[n] = 0x0707070707070707ull;
   if (v >= n) return;
   const uint32_t src = order[v];  // caller's id of device vertex v
   unsigned long long cols = 0;
@@ -261,7 +261,6 @@ __global__ void k_recolor(uint32_t n, int C, const uint8_t* __restrict__ in, uin
     }
   }
   reinterpret_cast<unsigned long long*>(out)[v] = cols;
-  if (out4) out4[v] = cols << 2;
 }
 
 // The kChiStride colours of vertex v (one 8-byte load) and colour slot c of them.
@@ -270,6 +269,14 @@ __device__ __forceinline__ uint64_t load_colors(const uint8_t* chi, uint32_t v) 
 }
 __device__ __forceinline__ uint32_t color_of(uint64_t cols, int c) {
   return static_cast<uint32_t>(cols >> (8 * c)) & 0xFFu;
+}
+// 1 << (4 * colour of slot c) from the half word holding slots c & ~3 .. c | 3:
+// the funnel shift uses the low 5 bits of its amount, and shifting the half
+// right by 8*(c&3) - 2 leaves 4 * colour there (colours < 8 leave bits 6-7 of
+// every byte zero, so nothing from the byte below leaks in).
+__device__ __forceinline__ uint32_t nibble_onehot(uint32_t half, int c) {
+  const uint32_t sh = (c & 3) ? (half >> (8 * (c & 3) - 2)) : (half << 2);
+  return __funnelshift_l(0u, 1u, sh);
 }
 
 // Degree-ordered orientation: out(x) = neighbours ranked below x, kept in id

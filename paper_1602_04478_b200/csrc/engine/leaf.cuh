@@ -21,6 +21,7 @@ struct LeafMapArgs {
   const uint64_t* off;
   const uint32_t* adj;
   const uint8_t* chi;  // [n][kChiStride], 0-based colours
+  uint32_t nv;  // vertex count = the dummy row of chi (colour 7 in every slot)
   const uint64_t* ub;  // node child on the leaf (row = img b), may be null
   const uint64_t* ua;  // node child on the boundary (row = img a), may be null
   uint32_t Pb, Pa, PZ, Pout;
@@ -234,56 +235,66 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
 // First leaf level (no child tables on either end): the row of x is, per
 // colouring, the colour histogram of x's neighbours without x's own colour —
 // entry of colour d is d - [d > chi x] (the squeezed rank of {d}).  For light
-// vertices (degree <= 256, k <= 8) a thread owns one vertex and counts all
-// colourings in registers: 4-bit fields (k <= 8 colours in one word) flushed
-// every 12 neighbours into 16-bit fields, as in the 3-cycle histograms.  No
-// shared memory, no atomics; vertices arrive in degree order, so a warp's
-// rows have similar lengths.
+// vertices (degree < 256, k <= 8) a thread owns one vertex and counts all
+// colourings in registers: 4-bit fields (one word per colouring holds all
+// colours; an entry adds 1 << (4 * colour), nibble_onehot) moved
+// every 12 neighbours into 8-bit fields, which hold any light row's counts.
+// The row is read with 16-byte loads, the next chunk in flight; for k < 8
+// slots past the row end count the dummy vertex (colour 7, unused), so the
+// loop has no branches.  No shared memory, no atomics; vertices arrive in
+// degree order, so a warp's rows have similar lengths.
+template <bool K8>
 __global__ void __launch_bounds__(256) leaf_hist_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist,
                                                         uint32_t nv) {
   const uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x;
   uint64_t upd = 0;
   if (gi < nv) {
     const uint32_t x = vlist[gi];
-    uint32_t N[kChiStride], H[kChiStride][4];
+    uint32_t N[kChiStride], Be[kChiStride], Bo[kChiStride];
 #pragma unroll
-    for (int c = 0; c < kChiStride; ++c) {
-      N[c] = 0;
-#pragma unroll
-      for (int w = 0; w < 4; ++w) H[c][w] = 0;
-    }
+    for (int c = 0; c < kChiStride; ++c) N[c] = Be[c] = Bo[c] = 0;
     auto flush = [&]() {
 #pragma unroll
       for (int c = 0; c < kChiStride; ++c) {
-        const uint32_t ev = N[c] & 0x0F0F0F0Fu, od = (N[c] >> 4) & 0x0F0F0F0Fu;
-#pragma unroll
-        for (int w = 0; w < 4; ++w) H[c][w] += ((ev >> (8 * w)) & 0xFFu) | (((od >> (8 * w)) & 0xFFu) << 16);
+        Be[c] += N[c] & 0x0F0F0F0Fu;
+        Bo[c] += (N[c] >> 4) & 0x0F0F0F0Fu;
         N[c] = 0;
       }
     };
     const uint64_t base = A.off[x], end = A.off[x + 1];
+    const uint64_t p0 = base & ~3ull;
+    const uint32_t head = static_cast<uint32_t>(base - p0), n = static_cast<uint32_t>(end - p0);
+    const uint32_t nch = (n + 3) >> 2;
+    // adj is padded by 16 bytes on upload
+    const uint4* src = reinterpret_cast<const uint4*>(A.adj + p0);
+    uint4 q = nch ? __ldg(src) : make_uint4(0, 0, 0, 0);
     int pend = 0;
-    // 16-byte loads of the row (adj is padded by 16 bytes on upload)
-    for (uint64_t p = base & ~3ull; p < end; p += 4) {
-      const uint4 q = __ldg(reinterpret_cast<const uint4*>(A.adj + p));
+    for (uint32_t ch = 0; ch < nch; ++ch) {
+      const uint4 qn = ch + 1 < nch ? __ldg(src + ch + 1) : q;
       const uint32_t ws[4] = {q.x, q.y, q.z, q.w};
       uint64_t cw[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) cw[u] = (p + u >= base && p + u < end) ? load_colors(A.chi, ws[u]) : ~0ull;
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t idx = 4 * ch + u;
+        const bool in = idx >= head && idx < n;
+        if (!K8) cw[u] = load_colors(A.chi, in ? ws[u] : A.nv);
+        else cw[u] = in ? load_colors(A.chi, ws[u]) : ~0ull;
+      }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        if (cw[u] == ~0ull) continue;
+        if (K8 && cw[u] == ~0ull) continue;
         const uint32_t lo32 = static_cast<uint32_t>(cw[u]), hi32 = static_cast<uint32_t>(cw[u] >> 32);
 #pragma unroll
         for (int c = 0; c < kChiStride; ++c) {
           const uint32_t half = c < 4 ? lo32 : hi32;
-          N[c] += 1u << (((half >> (8 * (c & 3))) & 7u) << 2);
+          N[c] += nibble_onehot(half, c);
         }
       }
       if (++pend == 3) {
         flush();
         pend = 0;
       }
+      q = qn;
     }
     flush();
     const uint64_t cxs = load_colors(A.chi, x);
@@ -294,7 +305,7 @@ __global__ void __launch_bounds__(256) leaf_hist_kernel(LeafMapArgs A, const uin
 #pragma unroll
       for (int d = 0; d < 8; ++d) {
         if (d >= A.k || d == static_cast<int>(cx)) continue;
-        const uint32_t v = (H[c][d >> 1] >> (16 * (d & 1))) & 0xFFFFu;
+        const uint32_t v = (((d & 1) ? Bo[c] : Be[c]) >> (8 * (d >> 1))) & 0xFFu;
         const uint32_t col = c * A.Pout + d - (d > static_cast<int>(cx) ? 1 : 0);
         st_entry(A.out, static_cast<uint64_t>(x) * A.rso + col, A.out_e, v);
         upd += v != 0;
@@ -472,23 +483,13 @@ __global__ void __launch_bounds__(256) leaf_pull_kernel(LeafMapArgs A, const uin
 // owns colouring slot t & 7 and every 32nd neighbour from t >> 3 (the 8 rows
 // of a neighbour are read by 8 consecutive lanes), private accumulators, then
 // the 32 partial rows of each colouring are summed in shared memory.
-template <int PB>
+template <int PB, int UNR>
 __global__ void __launch_bounds__(256) leaf_pull_heavy_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist,
                                                               uint32_t nv) {
   extern __shared__ u64 lsm[];
-  const uint32_t msize = leaf_map_size(A);
-  uint16_t* map = reinterpret_cast<uint16_t*>(lsm);
-  uint32_t* accs = reinterpret_cast<uint32_t*>(lsm + (msize * 2 + 7) / 8);
-  for (uint32_t i = threadIdx.x; i < msize; i += blockDim.x) {
-    const uint32_t ib = i % PB, cy = (i / PB) % A.k, cx = i / (PB * A.k);
-    uint16_t t = 0xFFFF;
-    if (cx != cy) {
-      const uint32_t fx = 1u << cx, fy = 1u << cy;
-      const uint32_t Mb = sig_expand(sig_unrank(c_lut, A.sb - 1, ib), fy);
-      if (!(Mb & fx)) t = static_cast<uint16_t>(sig_index(c_lut, Mb | fx, fx));
-    }
-    map[i] = t;
-  }
+  uint64_t* pmap = reinterpret_cast<uint64_t*>(lsm);
+  uint32_t* accs = reinterpret_cast<uint32_t*>(lsm + A.k * A.k);
+  build_pmap(A, PB, pmap);
   const uint32_t AS = A.Pout | 1u;
   uint32_t* acc = accs + threadIdx.x * AS;
   const int c = threadIdx.x & 7, jl = threadIdx.x >> 3;
@@ -499,18 +500,18 @@ __global__ void __launch_bounds__(256) leaf_pull_heavy_kernel(LeafMapArgs A, con
     for (uint32_t i = 0; i < A.Pout; ++i) acc[i] = 0;
     if (c < A.C) {
       const uint32_t cx = A.chi[static_cast<uint64_t>(x) * kChiStride + c];
-      const uint16_t* mx = map + cx * A.k * PB;
+      const uint64_t* mx = pmap + cx * A.k;
       const uint64_t base = A.off[x], end = A.off[x + 1];
-      for (uint64_t p = base + jl; p < end; p += 64) {
-        uint32_t y[2], cy[2], r[2][PB];
-        bool ok[2];
+      for (uint64_t p = base + jl; p < end; p += 32 * UNR) {
+        uint32_t y[UNR], cy[UNR], r[UNR][PB];
+        bool ok[UNR];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < UNR; ++u) {
           ok[u] = p + 32 * u < end;
           y[u] = ok[u] ? __ldg(A.adj + p + 32 * u) : 0u;
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < UNR; ++u) {
           cy[u] = ok[u] ? A.chi[static_cast<uint64_t>(y[u]) * kChiStride + c] : cx;
           const uint64_t roff = static_cast<uint64_t>(y[u]) * A.rsb + c * PB;
           if (A.ub_e == 2) {
@@ -522,14 +523,14 @@ __global__ void __launch_bounds__(256) leaf_pull_heavy_kernel(LeafMapArgs A, con
           }
         }
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < UNR; ++u) {
           if (cy[u] == cx) continue;
-          const uint16_t* my = mx + cy[u] * PB;
+          const uint64_t w = mx[cy[u]];
 #pragma unroll
           for (int e = 0; e < PB; ++e) {
-            const uint16_t t = my[e];
-            if (t == 0xFFFF || !r[u][e]) continue;
-            acc[t] += r[u][e];
+            const uint32_t t = static_cast<uint32_t>(w >> (5 * e)) & 31u;
+            if (t == 31u || !r[u][e]) continue;
+            atomicAdd(acc + t, r[u][e]);
             ++upd;
           }
         }

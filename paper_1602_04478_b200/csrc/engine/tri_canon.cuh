@@ -74,126 +74,17 @@ __device__ __forceinline__ void sfor(F&& f) {
 
 }  // namespace canon
 
-// Lane-mode register histogram of oriented edge j: H[c][w] holds the counts
-// of colours 2w and 2w+1 in colouring slot c as two 16-bit fields (lists are
-// shorter than 65536 in lane mode).  4-bit fields (all k <= 8 colours in one
-// word) are flushed into the 16-bit ones every 12 entries; the list is read
-// with 16-byte loads (cn_w is padded).
-__device__ __forceinline__ void lane_histogram(const TriHistArgs& A, uint64_t j, uint32_t (&H)[kChiStride][4]) {
-  uint32_t N[kChiStride];
-#pragma unroll
-  for (int c = 0; c < kChiStride; ++c) {
-    N[c] = 0;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) H[c][w] = 0;
-  }
-  auto flush = [&]() {
-#pragma unroll
-    for (int c = 0; c < kChiStride; ++c) {
-      const uint32_t ev = N[c] & 0x0F0F0F0Fu, od = (N[c] >> 4) & 0x0F0F0F0Fu;
-#pragma unroll
-      for (int w = 0; w < 4; ++w) H[c][w] += ((ev >> (8 * w)) & 0xFFu) | (((od >> (8 * w)) & 0xFFu) << 16);
-      N[c] = 0;
-    }
-  };
-  const uint64_t lo_ = A.cn_off[j], hi_ = A.cn_off[j + 1];
-  int pend = 0;
-  for (uint64_t p = lo_ & ~3ull; p < hi_; p += 4) {
-    const uint4 q = __ldg(reinterpret_cast<const uint4*>(A.cn_w + p));
-    const uint32_t ws[4] = {q.x, q.y, q.z, q.w};
-    uint64_t cw[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const bool in = p + u >= lo_ && p + u < hi_;
-      cw[u] = in ? load_colors(A.chi, ws[u]) : ~0ull;
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (cw[u] == ~0ull) continue;
-      const uint32_t lo32 = static_cast<uint32_t>(cw[u]), hi32 = static_cast<uint32_t>(cw[u] >> 32);
-#pragma unroll
-      for (int c = 0; c < kChiStride; ++c) {
-        const uint32_t half = c < 4 ? lo32 : hi32;
-        N[c] += 1u << (((half >> (8 * (c & 3))) & 7u) << 2);
-      }
-    }
-    if (++pend == 3) {
-      flush();
-      pend = 0;
-    }
-  }
-  flush();
-}
-
-// lane_histogram with the 16-byte list loads one chunk ahead (the next chunk is
-// in flight while the current one's colours are gathered and counted) and
-// colours pre-scaled by 4 (chi4): a colouring's count is one funnel shift and
-// one add.  For K < 8 entries past the list end count into the unused colour
-// 7 instead of being tested.
-template <int K>
-__device__ __forceinline__ void lane_histogram4(const TriHistArgs& A, uint64_t j, uint32_t (&H)[kChiStride][4]) {
-  uint32_t N[kChiStride];
-#pragma unroll
-  for (int c = 0; c < kChiStride; ++c) {
-    N[c] = 0;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) H[c][w] = 0;
-  }
-  auto flush = [&]() {
-#pragma unroll
-    for (int c = 0; c < kChiStride; ++c) {
-      const uint32_t ev = N[c] & 0x0F0F0F0Fu, od = (N[c] >> 4) & 0x0F0F0F0Fu;
-#pragma unroll
-      for (int w = 0; w < 4; ++w) H[c][w] += ((ev >> (8 * w)) & 0xFFu) | (((od >> (8 * w)) & 0xFFu) << 16);
-      N[c] = 0;
-    }
-  };
-  constexpr uint64_t kDummy = 0x1C1C1C1C1C1C1C1Cull;  // colour 7 (times 4) in every slot
-  const uint64_t lo_ = A.cn_off[j], hi_ = A.cn_off[j + 1];
-  uint64_t p = lo_ & ~3ull;
-  uint4 q = p < hi_ ? __ldg(reinterpret_cast<const uint4*>(A.cn_w + p)) : make_uint4(0, 0, 0, 0);
-  int pend = 0;
-  for (; p < hi_; p += 4) {
-    const uint4 qn = p + 4 < hi_ ? __ldg(reinterpret_cast<const uint4*>(A.cn_w + p + 4)) : q;
-    const uint32_t ws[4] = {q.x, q.y, q.z, q.w};
-    uint64_t cw[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const bool in = p + u >= lo_ && p + u < hi_;
-      cw[u] = in ? __ldg(A.chi4 + ws[u]) : (K < 8 ? kDummy : ~0ull);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (K == 8 && cw[u] == ~0ull) continue;
-      const uint32_t lo32 = static_cast<uint32_t>(cw[u]), hi32 = static_cast<uint32_t>(cw[u] >> 32);
-#pragma unroll
-      for (int c = 0; c < kChiStride; ++c) {
-        const uint32_t half = c < 4 ? lo32 : hi32;
-        // 1 << (4 * colour): the shift uses the low 5 bits, the byte holds 4 * colour < 32
-        N[c] += __funnelshift_l(0u, 1u, half >> (8 * (c & 3)));
-      }
-    }
-    if (++pend == 3) {
-      flush();
-      pend = 0;
-    }
-    q = qn;
-  }
-  flush();
-}
-
 // The lane's histogram row for oriented edge j, written to hrow[c*K + d]
 // (u16: lane-mode lists are shorter than 65536).  Three counter levels keep
 // the per-entry work to one funnel shift and one add per colouring:
 //   N[c]  4-bit fields, all colours of colouring slot c in one word (an entry
-//         adds 1 << (4 * colour); chi4 holds the colours pre-scaled by 4 and
-//         the shift uses the low 5 bits of the byte), moved every 12 entries
-//         into
+//         adds 1 << (4 * colour): one shift and one funnel shift,
+//         nibble_onehot), moved every 12 entries into
 //   B[c]  8-bit fields (even / odd colours), moved every 240 entries into
 //   hrow  the 16-bit row in shared memory (read-modify-write, rare).
 // The list is read with 16-byte loads, the next chunk in flight while the
 // current one is counted.  For K < 8 slots outside the list count vertex
-// A.nv, whose chi4 word is colour 7 (unused) in every slot, so the inner loop
+// A.nv, whose colours are 7 (unused) in every slot, so the inner loop
 // has no branches; for K = 8 they are skipped.
 template <int K>
 __device__ __forceinline__ void lane_histogram_row(const TriHistArgs& A, uint64_t j, uint16_t* hrow) {
@@ -236,8 +127,8 @@ __device__ __forceinline__ void lane_histogram_row(const TriHistArgs& A, uint64_
     for (int u = 0; u < 4; ++u) {
       const uint32_t idx = 4 * ch + u;
       const bool in = idx >= head && idx < n;
-      if (K < 8) cw[u] = __ldg(A.chi4 + (in ? ws[u] : A.nv));
-      else cw[u] = in ? __ldg(A.chi4 + ws[u]) : ~0ull;
+      if (K < 8) cw[u] = load_colors(A.chi, in ? ws[u] : A.nv);
+      else cw[u] = in ? load_colors(A.chi, ws[u]) : ~0ull;
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -246,7 +137,7 @@ __device__ __forceinline__ void lane_histogram_row(const TriHistArgs& A, uint64_
 #pragma unroll
       for (int c = 0; c < kChiStride; ++c) {
         const uint32_t half = c < 4 ? lo32 : hi32;
-        N[c] += __funnelshift_l(0u, 1u, half >> (8 * (c & 3)));
+        N[c] += nibble_onehot(half, c);
       }
     }
     if (++pend == 3) {

@@ -296,8 +296,7 @@ struct TriHistArgs {
   const uint32_t* out_slot;
   const uint32_t* rev;
   const uint8_t* chi;   // [n][kChiStride]
-  const uint64_t* chi4;  // the same colours times 4, one word per vertex (+ dummy vertex nv)
-  uint32_t nv;           // vertex count = index of chi4's dummy word (colour 7 in every slot)
+  uint32_t nv;           // vertex count = the dummy row of chi (colour 7 in every slot)
   int debug;             // MB_TRI_DEBUG timing split: 1 no join, 2 no list scan, 3 neither
   int t_safe;            // host bound: every fused-child entry < 2^44 (unchecked stage 2)
   int k, C;
