@@ -15,7 +15,7 @@
 // contiguous span.
 //
 // Degree-binned scheduling: a warp per light vertex, a 256-thread CTA per
-// heavy vertex (degree > 256), so hubs do not serialise a warp.
+// heavy vertex (degree >= 512), so hubs do not serialise a warp.
 
 struct LeafMapArgs {
   const uint64_t* off;
@@ -235,66 +235,56 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
 // First leaf level (no child tables on either end): the row of x is, per
 // colouring, the colour histogram of x's neighbours without x's own colour —
 // entry of colour d is d - [d > chi x] (the squeezed rank of {d}).  For light
-// vertices (degree < 256, k <= 8) a thread owns one vertex and counts all
-// colourings in registers: 4-bit fields (one word per colouring holds all
-// colours; an entry adds 1 << (4 * colour), nibble_onehot) moved
-// every 12 neighbours into 8-bit fields, which hold any light row's counts.
-// The row is read with 16-byte loads, the next chunk in flight; for k < 8
-// slots past the row end count the dummy vertex (colour 7, unused), so the
-// loop has no branches.  No shared memory, no atomics; vertices arrive in
-// degree order, so a warp's rows have similar lengths.
-template <bool K8>
+// vertices (degree < 512, k <= 8) a thread owns one vertex and counts all
+// colourings in registers: 4-bit fields (k <= 8 colours in one word) flushed
+// every 12 neighbours into 16-bit fields, as in the 3-cycle histograms.  No
+// shared memory, no atomics; vertices arrive in degree order, so a warp's
+// rows have similar lengths.
 __global__ void __launch_bounds__(256) leaf_hist_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist,
                                                         uint32_t nv) {
   const uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x;
   uint64_t upd = 0;
   if (gi < nv) {
     const uint32_t x = vlist[gi];
-    uint32_t N[kChiStride], Be[kChiStride], Bo[kChiStride];
+    uint32_t N[kChiStride], H[kChiStride][4];
 #pragma unroll
-    for (int c = 0; c < kChiStride; ++c) N[c] = Be[c] = Bo[c] = 0;
+    for (int c = 0; c < kChiStride; ++c) {
+      N[c] = 0;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) H[c][w] = 0;
+    }
     auto flush = [&]() {
 #pragma unroll
       for (int c = 0; c < kChiStride; ++c) {
-        Be[c] += N[c] & 0x0F0F0F0Fu;
-        Bo[c] += (N[c] >> 4) & 0x0F0F0F0Fu;
+        const uint32_t ev = N[c] & 0x0F0F0F0Fu, od = (N[c] >> 4) & 0x0F0F0F0Fu;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) H[c][w] += ((ev >> (8 * w)) & 0xFFu) | (((od >> (8 * w)) & 0xFFu) << 16);
         N[c] = 0;
       }
     };
     const uint64_t base = A.off[x], end = A.off[x + 1];
-    const uint64_t p0 = base & ~3ull;
-    const uint32_t head = static_cast<uint32_t>(base - p0), n = static_cast<uint32_t>(end - p0);
-    const uint32_t nch = (n + 3) >> 2;
-    // adj is padded by 16 bytes on upload
-    const uint4* src = reinterpret_cast<const uint4*>(A.adj + p0);
-    uint4 q = nch ? __ldg(src) : make_uint4(0, 0, 0, 0);
     int pend = 0;
-    for (uint32_t ch = 0; ch < nch; ++ch) {
-      const uint4 qn = ch + 1 < nch ? __ldg(src + ch + 1) : q;
+    // 16-byte loads of the row (adj is padded by 16 bytes on upload)
+    for (uint64_t p = base & ~3ull; p < end; p += 4) {
+      const uint4 q = __ldg(reinterpret_cast<const uint4*>(A.adj + p));
       const uint32_t ws[4] = {q.x, q.y, q.z, q.w};
       uint64_t cw[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t idx = 4 * ch + u;
-        const bool in = idx >= head && idx < n;
-        if (!K8) cw[u] = load_colors(A.chi, in ? ws[u] : A.nv);
-        else cw[u] = in ? load_colors(A.chi, ws[u]) : ~0ull;
-      }
+      for (int u = 0; u < 4; ++u) cw[u] = (p + u >= base && p + u < end) ? load_colors(A.chi, ws[u]) : ~0ull;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        if (K8 && cw[u] == ~0ull) continue;
+        if (cw[u] == ~0ull) continue;
         const uint32_t lo32 = static_cast<uint32_t>(cw[u]), hi32 = static_cast<uint32_t>(cw[u] >> 32);
 #pragma unroll
         for (int c = 0; c < kChiStride; ++c) {
           const uint32_t half = c < 4 ? lo32 : hi32;
-          N[c] += nibble_onehot(half, c);
+          N[c] += 1u << (((half >> (8 * (c & 3))) & 7u) << 2);
         }
       }
       if (++pend == 3) {
         flush();
         pend = 0;
       }
-      q = qn;
     }
     flush();
     const uint64_t cxs = load_colors(A.chi, x);
@@ -305,7 +295,7 @@ __global__ void __launch_bounds__(256) leaf_hist_kernel(LeafMapArgs A, const uin
 #pragma unroll
       for (int d = 0; d < 8; ++d) {
         if (d >= A.k || d == static_cast<int>(cx)) continue;
-        const uint32_t v = (((d & 1) ? Bo[c] : Be[c]) >> (8 * (d >> 1))) & 0xFFu;
+        const uint32_t v = (H[c][d >> 1] >> (16 * (d & 1))) & 0xFFFFu;
         const uint32_t col = c * A.Pout + d - (d > static_cast<int>(cx) ? 1 : 0);
         st_entry(A.out, static_cast<uint64_t>(x) * A.rso + col, A.out_e, v);
         upd += v != 0;
@@ -316,7 +306,8 @@ __global__ void __launch_bounds__(256) leaf_hist_kernel(LeafMapArgs A, const uin
   if ((threadIdx.x & 31) == 0 && upd) atomicAdd(A.updates, static_cast<u64>(upd));
 }
 
-// First leaf level for heavy vertices (degree > 256): a CTA per vertex, each
+
+// First leaf level for heavy vertices (degree >= 512): a CTA per vertex, each
 // thread counts a strided slice of the row in registers as leaf_hist_kernel
 // does, then the CTA sums the packed 16-bit counters (warp shuffles, then
 // across warps in shared memory).  Counts stay below 2^16 (the host checks
