@@ -485,15 +485,23 @@ inline size_t tri_canon_smem(int K, int S1, int FK, int SP, int out_kind, int po
 using TriCanonFn = void (*)(TriHistArgs);
 
 // The instantiated shapes (K, S1, FK, SP, NARROW); others use tri_hist_kernel.
+template <int K, int S1, int FK, int SP, bool N>
+constexpr TriCanonFn canon_ptr() {
+  if constexpr (S1 <= K && SP <= K && S1 >= 3 && (FK != 0 || S1 == 3) && K <= 8) return tri_canon_kernel<K, S1, FK, SP, N>;
+  else return nullptr;
+}
 inline TriCanonFn tri_canon_find(int K, int S1, int FK, int SP, bool narrow) {
 #define MB_CANON(k_, s_, f_, p_, n_) \
-  if (K == k_ && S1 == s_ && FK == f_ && SP == p_ && narrow == n_) return tri_canon_kernel<k_, s_, f_, p_, n_>;
+  if (K == k_ && S1 == s_ && FK == f_ && SP == p_ && narrow == n_) return canon_ptr<k_, s_, f_, p_, n_>();
 #define MB_CANON_K(k_)                                                                                    \
   MB_CANON(k_, 3, 0, 0, false) MB_CANON(k_, 3, 0, 4, false)                                               \
   MB_CANON(k_, 4, 1, 0, false) MB_CANON(k_, 4, 1, 0, true) MB_CANON(k_, 4, 2, 0, false)                   \
-  MB_CANON(k_, 4, 2, 0, true) MB_CANON(k_, 4, 3, 0, false)                                                \
+  MB_CANON(k_, 4, 2, 0, true) MB_CANON(k_, 4, 3, 0, false) \
   MB_CANON(k_, 5, 1, 6, false) MB_CANON(k_, 5, 1, 6, true) MB_CANON(k_, 5, 2, 6, false)                   \
   MB_CANON(k_, 5, 2, 6, true)
+  // k = 6 only (the config-1 query and its trees): each instance fully
+  // unrolls the 8-colouring join and costs ~30 s of compile time; other k use
+  // tri_hist_kernel
   MB_CANON_K(6)
 #undef MB_CANON_K
 #undef MB_CANON
