@@ -166,8 +166,13 @@ __device__ __forceinline__ void prefetch_span(const void* p, uint32_t bytes) {
 // K colours; S1 = this block's s_out; FK = pivot factor kind (0 none, 1 node
 // at P0, 2 node at P1, 3 edge (P0, P1)); SP = the fused parent's s_out (0: not
 // fused); NARROW = node factor stored as u32.
-template <int K, int S1, int FK, int SP, bool NARROW>
-__global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_canon_kernel(TriHistArgs A) {
+// BIL: fused shape whose host bound allows only the bilinear path (the
+// general two-stage code is not compiled in: fewer live registers).
+#ifndef MB_BIL_MINB
+#define MB_BIL_MINB MB_TRI_MINB
+#endif
+template <int K, int S1, int FK, int SP, bool NARROW, bool BIL = false>
+__global__ void __launch_bounds__(32 * kHistWarps, BIL ? MB_BIL_MINB : MB_TRI_MINB) tri_canon_kernel(TriHistArgs A) {
   constexpr int M = K - 2;                       // |R|
   constexpr int T1 = S1 - 2;                     // stage-1 subset size
   constexpr int P2 = canon::cbinom(M, T1);       // stage-1 entries
@@ -276,9 +281,10 @@ __global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_canon_kernel
     };
     FT Fc[2][NB];
     load_f(0, Fc);
-#pragma unroll
-    for (int c = 0; c < kChiStride; ++c) {
-      if (c >= C) break;
+    // rolled: the unrolled 8-colouring body overflowed the instruction cache
+    // (ncu: 16 % of stall samples "no_instructions")
+#pragma unroll 1
+    for (int c = 0; c < C; ++c) {
       FT Fn[2][NB];
       if (c + 1 < C) load_f(c + 1, Fn);  // in flight while colouring c is joined
       const uint32_t ca = color_of(cas, c), cb = color_of(cbs, c);
@@ -303,7 +309,7 @@ __global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_canon_kernel
         h[r] = hrow[c * K + d];
       }
       uint64_t acc = 0;
-      if (SP && A.t_safe) {
+      if (BIL || (SP && A.t_safe)) {
         // Fused child and parent as one bilinear form in h: with
         //   T[S] = sum_{r' in S} h[r'] F'[S \ r'],  U[A] = sum_{r in A} h[r] T[A \ r]
         // U[A] = 2 * sum over pairs {r, r'} in A of h[r] h[r'] F'[A \ {r, r'}].
@@ -355,7 +361,7 @@ __global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_canon_kernel
           pairs(0, Fc[1]);
           pairs(1, Fc[0]);
         }
-      } else {
+      } else if constexpr (!BIL) {
       uint64_t T[2][P2];
       uint64_t tmax = 0;
       // stage-1 products stay below 2^63 when every factor entry is < 2^44
@@ -445,8 +451,12 @@ __global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_canon_kernel
         }
       }
       }
-      local[c] += acc;
-      ovf |= local[c] < acc;
+#pragma unroll
+      for (int cc = 0; cc < kChiStride; ++cc)
+        if (cc == c) {
+          local[cc] += acc;
+          ovf |= local[cc] < acc;
+        }
       }
       if (c + 1 < C) {
 #pragma unroll
@@ -485,12 +495,17 @@ inline size_t tri_canon_smem(int K, int S1, int FK, int SP, int out_kind, int po
 using TriCanonFn = void (*)(TriHistArgs);
 
 // The instantiated shapes (K, S1, FK, SP, NARROW); others use tri_hist_kernel.
-template <int K, int S1, int FK, int SP, bool N>
+template <int K, int S1, int FK, int SP, bool N, bool BIL = false>
 constexpr TriCanonFn canon_ptr() {
-  if constexpr (S1 <= K && SP <= K && S1 >= 3 && (FK != 0 || S1 == 3) && K <= 8) return tri_canon_kernel<K, S1, FK, SP, N>;
+  if constexpr (S1 <= K && SP <= K && S1 >= 3 && (FK != 0 || S1 == 3) && K <= 8 && (!BIL || SP))
+    return tri_canon_kernel<K, S1, FK, SP, N, BIL>;
   else return nullptr;
 }
-inline TriCanonFn tri_canon_find(int K, int S1, int FK, int SP, bool narrow) {
+inline TriCanonFn tri_canon_find(int K, int S1, int FK, int SP, bool narrow, bool bil) {
+  if (bil) {  // the config-1 shapes
+    if (K == 6 && S1 == 5 && FK == 1 && SP == 6 && narrow) return canon_ptr<6, 5, 1, 6, true, true>();
+    if (K == 6 && S1 == 5 && FK == 2 && SP == 6 && narrow) return canon_ptr<6, 5, 2, 6, true, true>();
+  }
 #define MB_CANON(k_, s_, f_, p_, n_) \
   if (K == k_ && S1 == s_ && FK == f_ && SP == p_ && narrow == n_) return canon_ptr<k_, s_, f_, p_, n_>();
 #define MB_CANON_K(k_)                                                                                    \
