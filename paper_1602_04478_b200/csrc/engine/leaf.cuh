@@ -240,6 +240,8 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
 // every 12 neighbours into 16-bit fields, as in the 3-cycle histograms.  No
 // shared memory, no atomics; vertices arrive in degree order, so a warp's
 // rows have similar lengths.
+// K: the colour count when known at compile time (vector row stores), else 0.
+template <int K>
 __global__ void __launch_bounds__(256) leaf_hist_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist,
                                                         uint32_t nv) {
   const uint32_t gi = blockIdx.x * blockDim.x + threadIdx.x;
@@ -288,6 +290,25 @@ __global__ void __launch_bounds__(256) leaf_hist_kernel(LeafMapArgs A, const uin
     }
     flush();
     const uint64_t cxs = load_colors(A.chi, x);
+    if (K > 0 && A.out_e == 4) {
+      // the whole row (kChiStride colourings x (K-1) entries, 16-byte aligned)
+      // as 16-byte stores: entry e of colouring c is colour e or e + 1
+      // (squeezed past chi x), a select between two static fields
+      constexpr int P = K > 0 ? K - 1 : 1, W = kChiStride * P;
+      uint4* orow = reinterpret_cast<uint4*>(reinterpret_cast<uint32_t*>(A.out) + static_cast<uint64_t>(x) * A.rso);
+      uint32_t q[4];
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const int c = w / P, e = w % P;
+        const uint32_t cx = color_of(cxs, c);
+        const uint32_t lo = (H[c][e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+        const uint32_t hi = (H[c][(e + 1) >> 1] >> (16 * ((e + 1) & 1))) & 0xFFFFu;
+        const uint32_t v = c < A.C ? (static_cast<uint32_t>(e) >= cx ? hi : lo) : 0u;
+        upd += v != 0;
+        q[w & 3] = v;
+        if ((w & 3) == 3) orow[w >> 2] = make_uint4(q[0], q[1], q[2], q[3]);
+      }
+    } else {
 #pragma unroll
     for (int c = 0; c < kChiStride; ++c) {
       if (c >= A.C) break;
@@ -300,6 +321,7 @@ __global__ void __launch_bounds__(256) leaf_hist_kernel(LeafMapArgs A, const uin
         st_entry(A.out, static_cast<uint64_t>(x) * A.rso + col, A.out_e, v);
         upd += v != 0;
       }
+    }
     }
   }
   for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(0xffffffffu, upd, o);
