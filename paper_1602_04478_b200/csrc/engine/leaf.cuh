@@ -290,7 +290,24 @@ __global__ void __launch_bounds__(256) leaf_hist_kernel(LeafMapArgs A, const uin
     }
     flush();
     const uint64_t cxs = load_colors(A.chi, x);
-    if (K > 0 && A.out_e == 4) {
+    if (K > 0 && A.out_e == 2) {
+      // u16 row: two entries per word
+      constexpr int P = K > 0 ? K - 1 : 1, W = kChiStride * P;
+      uint4* orow = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(A.out) + static_cast<uint64_t>(x) * A.rso);
+      uint32_t q[4];
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const int c = w / P, e = w % P;
+        const uint32_t cx = color_of(cxs, c);
+        const uint32_t lo = (H[c][e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+        const uint32_t hi = (H[c][(e + 1) >> 1] >> (16 * ((e + 1) & 1))) & 0xFFFFu;
+        const uint32_t v = c < A.C ? (static_cast<uint32_t>(e) >= cx ? hi : lo) : 0u;
+        upd += v != 0;
+        if (w & 1) q[(w >> 1) & 3] |= v << 16;
+        else q[(w >> 1) & 3] = v;
+        if ((w & 7) == 7) orow[w >> 3] = make_uint4(q[0], q[1], q[2], q[3]);
+      }
+    } else if (K > 0 && A.out_e == 4) {
       // the whole row (kChiStride colourings x (K-1) entries, 16-byte aligned)
       // as 16-byte stores: entry e of colouring c is colour e or e + 1
       // (squeezed past chi x), a select between two static fields
