@@ -469,13 +469,22 @@ __global__ void __launch_bounds__(256) leaf_pull_kernel(LeafMapArgs A, const uin
     const uint32_t cx = A.chi[static_cast<uint64_t>(x) * kChiStride + c];
     const uint64_t* mx = pmap + cx * A.k;
     const uint64_t base = A.off[x], end = A.off[x + 1];
+    // neighbour ids one group ahead: the colour and row gathers of a group
+    // do not wait behind its own id loads
+    uint32_t yn[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) yn[u] = base + u < end ? __ldg(A.adj + base + u) : 0u;
     for (uint64_t p = base; p < end; p += UNR) {
       uint32_t y[UNR], cy[UNR], r[UNR][PB];
       bool ok[UNR];
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
         ok[u] = p + u < end;
-        y[u] = ok[u] ? __ldg(A.adj + p + u) : 0u;
+        y[u] = yn[u];
+      }
+      if (p + UNR < end) {
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) yn[u] = p + UNR + u < end ? __ldg(A.adj + p + UNR + u) : 0u;
       }
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
