@@ -279,6 +279,19 @@ __device__ __forceinline__ uint32_t nibble_onehot(uint32_t half, int c) {
   return __funnelshift_l(0u, 1u, sh);
 }
 
+// Edge metadata in list-length order (eorder): meta[i] = (a, b, slot a->b,
+// slot b->a) and range[i] = the CN list [lo, hi) of oriented edge eorder[i].
+__global__ void k_edge_meta(uint64_t no, const uint32_t* __restrict__ eorder, const uint32_t* __restrict__ src,
+                            const uint32_t* __restrict__ nbr, const uint32_t* __restrict__ slot,
+                            const uint32_t* __restrict__ rev, const uint64_t* __restrict__ cn_off,
+                            uint4* __restrict__ meta, ulonglong2* __restrict__ range) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= no) return;
+  const uint32_t j = eorder[i], s = slot[j];
+  meta[i] = make_uint4(src[j], nbr[j], s, rev[s]);
+  range[i] = make_ulonglong2(cn_off[j], cn_off[j + 1]);
+}
+
 // Degree-ordered orientation: out(x) = neighbours ranked below x, kept in id
 // order, remembered with their CSR slot.
 __global__ void k_out_degree(uint32_t n, const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,

@@ -87,7 +87,7 @@ __device__ __forceinline__ void sfor(F&& f) {
 // A.nv, whose colours are 7 (unused) in every slot, so the inner loop
 // has no branches; for K = 8 they are skipped.
 template <int K>
-__device__ __forceinline__ void lane_histogram_row(const TriHistArgs& A, uint64_t j, uint16_t* hrow) {
+__device__ __forceinline__ void lane_histogram_row(const TriHistArgs& A, uint64_t lo, uint64_t hi, uint16_t* hrow) {
   uint32_t N[kChiStride], Be[kChiStride], Bo[kChiStride];
 #pragma unroll
   for (int c = 0; c < kChiStride; ++c) N[c] = Be[c] = Bo[c] = 0;
@@ -112,7 +112,6 @@ __device__ __forceinline__ void lane_histogram_row(const TriHistArgs& A, uint64_
     }
     spilled = true;
   };
-  const uint64_t lo = A.cn_off[j], hi = A.cn_off[j + 1];
   const uint64_t p0 = lo & ~3ull;
   const uint32_t head = static_cast<uint32_t>(lo - p0), n = static_cast<uint32_t>(hi - p0);
   const uint32_t nch = (n + 3) >> 2;
@@ -228,9 +227,9 @@ __global__ void __launch_bounds__(32 * kHistWarps, BIL ? MB_BIL_MINB : MB_TRI_MI
        bt += static_cast<uint64_t>(gridDim.x) * kHistWarps) {
     const uint64_t jj = bt * 32 + lane;
     if (jj >= A.nitems) continue;
-    const uint64_t j = A.eorder[jj];
-    const uint32_t a = A.out_src[j], b = A.out_nbr[j];
-    const uint32_t sab = A.out_slot[j], sba = A.rev[sab];
+    const uint4 em = A.emeta[jj];
+    const ulonglong2 er = A.erange[jj];
+    const uint32_t a = em.x, b = em.y, sab = em.z, sba = em.w;
     // the pivot factor rows are gathered after the list scan: start their
     // trip to L2 now
     if (FK == 1 || FK == 2) {
@@ -243,7 +242,7 @@ __global__ void __launch_bounds__(32 * kHistWarps, BIL ? MB_BIL_MINB : MB_TRI_MI
       prefetch_span(F + static_cast<uint64_t>(sab) * A.rsF * 8u, fbytes);
       prefetch_span(F + static_cast<uint64_t>(sba) * A.rsF * 8u, fbytes);
     }
-    if (!(A.debug & 2)) lane_histogram_row<K>(A, j, hrow);
+    if (!(A.debug & 2)) lane_histogram_row<K>(A, er.x, er.y, hrow);
     if (A.debug & 1) continue;
     const uint64_t cas = load_colors(A.chi, a), cbs = load_colors(A.chi, b);
     uint32_t updl = 0;

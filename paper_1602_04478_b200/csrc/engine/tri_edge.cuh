@@ -304,6 +304,8 @@ struct TriHistArgs {
   int f_safe;               // host bound: every factor entry < 2^44 (lane mode: unchecked terms)
   int F_n;                  // pivot factor stored narrow (u32)            // 1: lane per edge, register counters (k <= 8, lists < 65536)
   const uint32_t* eorder;   // oriented edges in CN-length order (lane_mode)
+  const uint4* emeta;       // (a, b, slot a->b, slot b->a) per eorder position
+  const ulonglong2* erange; // CN list [lo, hi) per eorder position
   // stage 1: this block
   int s_out;
   uint32_t P2;          // C(k-2, s_out-2): entries of S containing both pivot colours
