@@ -254,8 +254,9 @@ __global__ void __launch_bounds__(32 * kHistWarps, BIL ? MB_BIL_MINB : MB_TRI_MI
 #pragma unroll
       for (int o = 0; o < 2; ++o) {
         const uint32_t c0 = o ? cb : ca, c1 = o ? ca : cb;
-        if (FK == 0) {
-          Fo[o][0] = 1;
+        if (FK == 0 || (A.debug & 4)) {
+#pragma unroll
+          for (int q = 0; q < NB; ++q) Fo[o][q] = 1;
         } else if (ca == cb) {
 #pragma unroll
           for (int q = 0; q < NB; ++q) Fo[o][q] = 0;

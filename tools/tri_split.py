@@ -14,7 +14,7 @@ for _ in range(5): mb.count_colorful(g, plan, chi)
 for name, ms, n, b in mb.engine_timings(g):
     if name.startswith('tri'): print(name, round(ms / 5, 4))
 '''
-for mode in ["0", "1", "2", "3"]:
+for mode in sys.argv[1:] or ["0", "1", "2", "3"]:
     env = dict(os.environ, MB_TRI_DEBUG=mode)
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True)
     print("mode", mode, out.stdout.strip(), out.stderr.strip()[-300:])
