@@ -153,15 +153,6 @@ __device__ __forceinline__ void lane_histogram_row(const TriHistArgs& A, uint64_
   flushB();
 }
 
-__device__ __forceinline__ void prefetch_l2(const void* p) {
-  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
-}
-__device__ __forceinline__ void prefetch_span(const void* p, uint32_t bytes) {
-  const char* c = static_cast<const char*>(p);
-  for (uint32_t o = 0; o < bytes; o += 128) prefetch_l2(c + o);
-  prefetch_l2(c + bytes - 1);
-}
-
 // K colours; S1 = this block's s_out; FK = pivot factor kind (0 none, 1 node
 // at P0, 2 node at P1, 3 edge (P0, P1)); SP = the fused parent's s_out (0: not
 // fused); NARROW = node factor stored as u32.
@@ -222,26 +213,21 @@ __global__ void __launch_bounds__(32 * kHistWarps, BIL ? MB_BIL_MINB : MB_TRI_MI
   for (int c = 0; c < kChiStride; ++c) local[c] = 0;
   uint64_t upd = 0;
   const uint64_t nbatch = (A.nitems + 31) / 32;
-  const uint32_t fbytes = FK ? static_cast<uint32_t>(C) * A.PF * (NARROW ? 4u : 8u) : 0u;
-  for (uint64_t bt = static_cast<uint64_t>(blockIdx.x) * kHistWarps + wid; bt < nbatch;
-       bt += static_cast<uint64_t>(gridDim.x) * kHistWarps) {
+  // edge metadata one iteration ahead (its DRAM latency would otherwise
+  // stall every edge)
+  const uint64_t bstride = static_cast<uint64_t>(gridDim.x) * kHistWarps;
+  uint64_t bt = static_cast<uint64_t>(blockIdx.x) * kHistWarps + wid;
+  uint4 emn = make_uint4(0, 0, 0, 0);
+  ulonglong2 ern = make_ulonglong2(0, 0);
+  if (bt * 32 + lane < A.nitems) emn = A.emeta[bt * 32 + lane], ern = A.erange[bt * 32 + lane];
+  for (; bt < nbatch; bt += bstride) {
     const uint64_t jj = bt * 32 + lane;
+    const uint4 em = emn;
+    const ulonglong2 er = ern;
+    const uint64_t jn = jj + bstride * 32;
+    if (jn < A.nitems) emn = A.emeta[jn], ern = A.erange[jn];
     if (jj >= A.nitems) continue;
-    const uint4 em = A.emeta[jj];
-    const ulonglong2 er = A.erange[jj];
     const uint32_t a = em.x, b = em.y, sab = em.z, sba = em.w;
-    // the pivot factor rows are gathered after the list scan: start their
-    // trip to L2 now
-    if (FK == 1 || FK == 2) {
-      const char* F = reinterpret_cast<const char*>(A.F);
-      const uint32_t rb = A.rsF * (NARROW ? 4u : 8u);
-      prefetch_span(F + static_cast<uint64_t>(a) * rb, fbytes);
-      prefetch_span(F + static_cast<uint64_t>(b) * rb, fbytes);
-    } else if (FK == 3) {
-      const char* F = reinterpret_cast<const char*>(A.F);
-      prefetch_span(F + static_cast<uint64_t>(sab) * A.rsF * 8u, fbytes);
-      prefetch_span(F + static_cast<uint64_t>(sba) * A.rsF * 8u, fbytes);
-    }
     if (!(A.debug & 2)) lane_histogram_row<K>(A, er.x, er.y, hrow);
     if (A.debug & 1) continue;
     const uint64_t cas = load_colors(A.chi, a), cbs = load_colors(A.chi, b);
