@@ -175,13 +175,17 @@ __global__ void __launch_bounds__(32 * kHistWarps, BIL ? MB_BIL_MINB : MB_TRI_MI
   // per-CTA maps: fmap[(cf*K + cx)*NB + j] = row index, in the node factor keyed
   // by colour cf, of the j-th (T1-1)-subset of R = [K] \ {cf, cx};
   // idx1/idx1p[(c0*K + c1)*P + i] = unary-output index of relative entry i
-  constexpr int FMAP = (FK == 1 || FK == 2) ? K * K * NB : 0;
+  // rows of <= 16 entries: the NB indices of a colour pair packed 4 bits each in one word
+  constexpr bool PACK = (FK == 1 || FK == 2) && NB <= 8 && canon::cbinom(K - 1, T1 - 1) <= 16;
+  constexpr int FMAP = (FK == 1 || FK == 2) ? K * K * (NB > 4 ? NB : 4) : 0;
   uint8_t* fmap = reinterpret_cast<uint8_t*>(hsm);
   uint16_t* idx1 = reinterpret_cast<uint16_t*>(hsm + (FMAP + 3) / 4);
   const int n1 = A.out_kind == 1 ? K * K * P2 : 0;
   uint16_t* idx1p = idx1 + n1;
   const int n1p = (SP && A.pout_kind == 1) ? K * K * P2p : 0;
   uint16_t* hist16_base = idx1p + n1p + ((n1 + n1p) & 1);  // 4-byte aligned
+  for (int i = threadIdx.x; i < (FMAP + 3) / 4; i += blockDim.x) hsm[i] = 0;
+  __syncthreads();
   for (int e = threadIdx.x; e < K * K * (NB + P2 + P2p); e += blockDim.x) {
     // one pass over (c0, c1, slot) triples fills whichever maps this launch needs
     const int q = e / (K * K), pr = e % (K * K), c0 = pr / K, c1 = pr % K;
@@ -190,7 +194,9 @@ __global__ void __launch_bounds__(32 * kHistWarps, BIL ? MB_BIL_MINB : MB_TRI_MI
     if (q < NB) {
       if (FMAP) {
         const uint32_t S = sig_expand(sig_unrank(c_lut, T1 - 1, q), f2) & ~(1u << c1);
-        fmap[pr * NB + q] = static_cast<uint8_t>(sig_index(c_lut, S, 1u << c0));
+        const uint32_t ix = sig_index(c_lut, S, 1u << c0);
+        if (PACK) atomicOr(reinterpret_cast<uint32_t*>(fmap) + pr, ix << (4 * q));
+        else fmap[pr * NB + q] = static_cast<uint8_t>(ix);
       }
     } else if (q < NB + P2) {
       const int i = q - NB;
@@ -255,10 +261,11 @@ __global__ void __launch_bounds__(32 * kHistWarps, BIL ? MB_BIL_MINB : MB_TRI_MI
           const uint32_t v = FK == 1 ? (o ? b : a) : (o ? a : b);
           const uint32_t cf = FK == 1 ? c0 : c1, cx = FK == 1 ? c1 : c0;
           const uint8_t* mp = fmap + (cf * K + cx) * NB;
+          const uint32_t pk = PACK ? reinterpret_cast<const uint32_t*>(fmap)[cf * K + cx] : 0u;
           const uint64_t ro = static_cast<uint64_t>(v) * A.rsF + c * A.PF;
 #pragma unroll
           for (int q = 0; q < NB; ++q) {
-            const uint32_t ix = mp[q];
+            const uint32_t ix = PACK ? (pk >> (4 * q)) & 15u : mp[q];
             if (NARROW) Fo[o][q] = static_cast<FT>(__ldg(reinterpret_cast<const uint32_t*>(A.F) + ro + ix));
             else Fo[o][q] = static_cast<FT>(__ldg(A.F + ro + ix));
           }
@@ -471,7 +478,7 @@ __global__ void __launch_bounds__(32 * kHistWarps, BIL ? MB_BIL_MINB : MB_TRI_MI
 inline size_t tri_canon_smem(int K, int S1, int FK, int SP, int out_kind, int pout_kind) {
   auto bn = [](int n, int r) { return canon::cbinom(n, r); };
   const int M = K - 2, NB = FK ? bn(M, S1 - 3) : 1, P2 = bn(M, S1 - 2), P2p = SP ? bn(M, SP - 2) : 0;
-  const int FMAP = (FK == 1 || FK == 2) ? K * K * NB : 0;
+  const int FMAP = (FK == 1 || FK == 2) ? K * K * (NB > 4 ? NB : 4) : 0;
   const int n1 = out_kind == 1 ? K * K * P2 : 0, n1p = (SP && pout_kind == 1) ? K * K * P2p : 0;
   const size_t LS = 2 * ((((kChiStride * K) + 1) / 2) | 1);
   return static_cast<size_t>((FMAP + 3) / 4) * 4 + 2 * static_cast<size_t>(n1 + n1p + ((n1 + n1p) & 1)) +
