@@ -28,6 +28,7 @@ struct LeafMapArgs {
   uint32_t rsb, rsa, rso;  // row strides (C_alloc * P)
   int sb, sa, sZ, k, C;
   int unchecked;  // entries provably < 2^62 (host bound): plain adds
+  uint32_t psb, psa, pso;  // per-colouring row strides: P, or 8 for padded u16 rows (bind())
   int ub_e, ua_e, out_e;  // entry bytes of the tables: 8, or narrow 4 (u32) / 2 (u16), see bind()
   uint64_t* out;
   int* err;
@@ -120,7 +121,7 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
           cy[u] = ok[u] ? A.chi[static_cast<uint64_t>(y[u]) * kChiStride + cc[u]] : 0xFFu;
-          const uint64_t roff = static_cast<uint64_t>(y[u]) * A.rsb + cc[u] * PBc;
+          const uint64_t roff = static_cast<uint64_t>(y[u]) * A.rsb + cc[u] * A.psb;
           if (A.ub_e == 2) {
 #pragma unroll
             for (int e = 0; e < PBc; ++e) r[u][e] = ok[u] ? ld_entry(A.ub, roff + e, 2) : 0u;
@@ -162,7 +163,7 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
         continue;
       }
       if (cy == cx) continue;
-      const uint64_t roff = static_cast<uint64_t>(y) * A.rsb + c * pb;
+      const uint64_t roff = static_cast<uint64_t>(y) * A.rsb + c * A.psb;
       for (uint32_t i0 = 0; i0 < pb; i0 += 8) {
         // the row's loads are issued together, then consumed
         uint64_t r[8];
@@ -201,7 +202,8 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
     }
     if (!A.ua) {
       for (uint32_t i = lane; i < A.C * A.Pout; i += GROUP)
-        st_entry(A.out, static_cast<uint64_t>(x) * A.rso + i, A.out_e, static_cast<uint64_t>(Z[i]));
+        st_entry(A.out, static_cast<uint64_t>(x) * A.rso + (i / A.Pout) * A.pso + i % A.Pout, A.out_e,
+                 static_cast<uint64_t>(Z[i]));
     } else {
       const uint64_t per = static_cast<uint64_t>(A.PZ) * A.Pa;
       for (uint64_t it = lane; it < per * A.C; it += GROUP) {
@@ -210,7 +212,7 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
         const uint32_t iz = static_cast<uint32_t>(r / A.Pa), ia = static_cast<uint32_t>(r - iz * A.Pa);
         const uint64_t z = Z[c * A.PZ + iz];
         if (!z) continue;
-        const uint64_t aoff = static_cast<uint64_t>(x) * A.rsa + c * A.Pa + ia;
+        const uint64_t aoff = static_cast<uint64_t>(x) * A.rsa + c * A.psa + ia;
         const uint64_t a = ld_entry(A.ua, aoff, A.ua_e);
         if (!a) continue;
         const uint32_t fx = 1u << color_of(cxs, c);
@@ -224,7 +226,8 @@ leaf_map_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist, uint32_t nv) 
       }
       if (GROUP == 32) __syncwarp(); else __syncthreads();
       for (uint32_t i = lane; i < A.C * A.Pout; i += GROUP)
-        st_entry(A.out, static_cast<uint64_t>(x) * A.rso + i, A.out_e, static_cast<uint64_t>(O[i]));
+        st_entry(A.out, static_cast<uint64_t>(x) * A.rso + (i / A.Pout) * A.pso + i % A.Pout, A.out_e,
+                 static_cast<uint64_t>(O[i]));
     }
     if (GROUP == 32) __syncwarp(); else __syncthreads();
   }
@@ -290,7 +293,25 @@ __global__ void __launch_bounds__(256) leaf_hist_kernel(LeafMapArgs A, const uin
     }
     flush();
     const uint64_t cxs = load_colors(A.chi, x);
-    if (K > 0 && A.out_e == 2) {
+    if (K > 0 && K <= 9 && A.out_e == 2 && A.pso == 8) {
+      // padded u16 row: one 16-byte store per colouring (entries past K-1 are 0)
+      constexpr int P = K > 0 ? K - 1 : 1;
+      uint4* orow = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(A.out) + static_cast<uint64_t>(x) * A.rso);
+#pragma unroll
+      for (int c = 0; c < kChiStride; ++c) {
+        const uint32_t cx = color_of(cxs, c);
+        uint32_t q[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int e = 0; e < P && e < 8; ++e) {
+          const uint32_t lo = (H[c][e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+          const uint32_t hi = (H[c][(e + 1) >> 1] >> (16 * ((e + 1) & 1))) & 0xFFFFu;
+          const uint32_t v = c < A.C ? (static_cast<uint32_t>(e) >= cx ? hi : lo) : 0u;
+          upd += v != 0;
+          q[e >> 1] |= v << (16 * (e & 1));
+        }
+        orow[c] = make_uint4(q[0], q[1], q[2], q[3]);
+      }
+    } else if (K > 0 && A.out_e == 2 && A.pso == A.Pout) {
       // u16 row: two entries per word
       constexpr int P = K > 0 ? K - 1 : 1, W = kChiStride * P;
       uint4* orow = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(A.out) + static_cast<uint64_t>(x) * A.rso);
@@ -307,7 +328,7 @@ __global__ void __launch_bounds__(256) leaf_hist_kernel(LeafMapArgs A, const uin
         else q[(w >> 1) & 3] = v;
         if ((w & 7) == 7) orow[w >> 3] = make_uint4(q[0], q[1], q[2], q[3]);
       }
-    } else if (K > 0 && A.out_e == 4) {
+    } else if (K > 0 && A.out_e == 4 && A.pso == A.Pout) {
       // the whole row (kChiStride colourings x (K-1) entries, 16-byte aligned)
       // as 16-byte stores: entry e of colouring c is colour e or e + 1
       // (squeezed past chi x), a select between two static fields
@@ -334,7 +355,7 @@ __global__ void __launch_bounds__(256) leaf_hist_kernel(LeafMapArgs A, const uin
       for (int d = 0; d < 8; ++d) {
         if (d >= A.k || d == static_cast<int>(cx)) continue;
         const uint32_t v = (H[c][d >> 1] >> (16 * (d & 1))) & 0xFFFFu;
-        const uint32_t col = c * A.Pout + d - (d > static_cast<int>(cx) ? 1 : 0);
+        const uint32_t col = c * A.pso + d - (d > static_cast<int>(cx) ? 1 : 0);
         st_entry(A.out, static_cast<uint64_t>(x) * A.rso + col, A.out_e, v);
         upd += v != 0;
       }
@@ -410,7 +431,7 @@ __global__ void __launch_bounds__(256) leaf_hist_heavy_kernel(LeafMapArgs A, con
 #pragma unroll
           for (int w = 0; w < 8; ++w) v += red[w][c * 4 + (d >> 1)];
           v = (v >> (16 * (d & 1))) & 0xFFFFu;
-          st_entry(A.out, static_cast<uint64_t>(x) * A.rso + c * A.Pout + d - (d > static_cast<int>(cx) ? 1 : 0),
+          st_entry(A.out, static_cast<uint64_t>(x) * A.rso + c * A.pso + d - (d > static_cast<int>(cx) ? 1 : 0),
                    A.out_e, v);
           upd += v != 0;
         }
@@ -489,8 +510,15 @@ __global__ void __launch_bounds__(256) leaf_pull_kernel(LeafMapArgs A, const uin
 #pragma unroll
       for (int u = 0; u < UNR; ++u) {
         cy[u] = ok[u] ? A.chi[static_cast<uint64_t>(y[u]) * kChiStride + c] : cx;
-        const uint64_t roff = static_cast<uint64_t>(y[u]) * A.rsb + c * PB;
-        if (A.ub_e == 2) {
+        const uint64_t roff = static_cast<uint64_t>(y[u]) * A.rsb + c * A.psb;
+        if (PB <= 8 && A.ub_e == 2 && A.psb == 8) {
+          // padded u16 row: one 16-byte load
+          const uint4 v4 = ok[u] ? __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(A.ub) + roff))
+                                 : make_uint4(0, 0, 0, 0);
+          const uint32_t wv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+          for (int e = 0; e < PB; ++e) r[u][e] = (wv[(e >> 1) & 3] >> (16 * (e & 1))) & 0xFFFFu;
+        } else if (A.ub_e == 2) {
 #pragma unroll
           for (int e = 0; e < PB; ++e) r[u][e] = ok[u] ? ld_entry(A.ub, roff + e, 2) : 0u;
         } else {
@@ -512,7 +540,7 @@ __global__ void __launch_bounds__(256) leaf_pull_kernel(LeafMapArgs A, const uin
       }
     }
     for (uint32_t i = 0; i < A.Pout; ++i)
-      st_entry(A.out, static_cast<uint64_t>(x) * A.rso + c * A.Pout + i, A.out_e, acc[i]);
+      st_entry(A.out, static_cast<uint64_t>(x) * A.rso + c * A.pso + i, A.out_e, acc[i]);
   }
   for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(0xffffffffu, upd, o);
   if ((threadIdx.x & 31) == 0 && upd) atomicAdd(A.updates, static_cast<u64>(upd));
@@ -552,8 +580,15 @@ __global__ void __launch_bounds__(256) leaf_pull_heavy_kernel(LeafMapArgs A, con
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
           cy[u] = ok[u] ? A.chi[static_cast<uint64_t>(y[u]) * kChiStride + c] : cx;
-          const uint64_t roff = static_cast<uint64_t>(y[u]) * A.rsb + c * PB;
-          if (A.ub_e == 2) {
+          const uint64_t roff = static_cast<uint64_t>(y[u]) * A.rsb + c * A.psb;
+          if (PB <= 8 && A.ub_e == 2 && A.psb == 8) {
+            // padded u16 row: one 16-byte load
+            const uint4 v4 = ok[u] ? __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(A.ub) + roff))
+                                   : make_uint4(0, 0, 0, 0);
+            const uint32_t wv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+            for (int e = 0; e < PB; ++e) r[u][e] = (wv[(e >> 1) & 3] >> (16 * (e & 1))) & 0xFFFFu;
+          } else if (A.ub_e == 2) {
 #pragma unroll
             for (int e = 0; e < PB; ++e) r[u][e] = ok[u] ? ld_entry(A.ub, roff + e, 2) : 0u;
           } else {
@@ -580,7 +615,7 @@ __global__ void __launch_bounds__(256) leaf_pull_heavy_kernel(LeafMapArgs A, con
       const uint32_t cc = o / A.Pout, i = o - cc * A.Pout;
       uint32_t s = 0;
       for (int l = 0; l < 32; ++l) s += accs[(l * 8 + cc) * AS + i];
-      st_entry(A.out, static_cast<uint64_t>(x) * A.rso + o, A.out_e, s);
+      st_entry(A.out, static_cast<uint64_t>(x) * A.rso + cc * A.pso + i, A.out_e, s);
     }
   }
   for (int o = 16; o > 0; o >>= 1) upd += __shfl_down_sync(0xffffffffu, upd, o);
