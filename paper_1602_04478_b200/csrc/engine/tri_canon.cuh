@@ -86,6 +86,9 @@ __device__ __forceinline__ void sfor(F&& f) {
 // current one is counted.  For K < 8 slots outside the list count vertex
 // A.nv, whose colours are 7 (unused) in every slot, so the inner loop
 // has no branches; for K = 8 they are skipped.
+#ifndef MB_HIST_PIPE
+#define MB_HIST_PIPE 1  // measured 0.876 vs 0.896 ms per config-1 batch
+#endif
 template <int K>
 __device__ __forceinline__ void lane_histogram_row(const TriHistArgs& A, uint64_t lo, uint64_t hi, uint16_t* hrow) {
   uint32_t N[kChiStride], Be[kChiStride], Bo[kChiStride];
@@ -116,8 +119,54 @@ __device__ __forceinline__ void lane_histogram_row(const TriHistArgs& A, uint64_
   const uint32_t head = static_cast<uint32_t>(lo - p0), n = static_cast<uint32_t>(hi - p0);
   const uint32_t nch = (n + 3) >> 2;
   const uint4* src = reinterpret_cast<const uint4*>(A.cn_w + p0);
-  uint4 q = nch ? __ldg(src) : make_uint4(0, 0, 0, 0);
   int pend = 0, nfl = 0;
+#if MB_HIST_PIPE
+  // two-stage pipeline: list chunk ch+2 and the colours of chunk ch+1 are in
+  // flight while chunk ch is counted
+  auto gather = [&](const uint4& qq, uint32_t ch, uint64_t (&cw)[4]) {
+    const uint32_t ws[4] = {qq.x, qq.y, qq.z, qq.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t idx = 4 * ch + u;
+      const bool in = idx >= head && idx < n;
+      if (K < 8) cw[u] = load_colors(A.chi, in ? ws[u] : A.nv);
+      else cw[u] = in ? load_colors(A.chi, ws[u]) : ~0ull;
+    }
+  };
+  uint4 q1 = nch > 1 ? __ldg(src + 1) : make_uint4(0, 0, 0, 0);
+  uint64_t cwc[4];
+  {
+    const uint4 q0 = nch ? __ldg(src) : make_uint4(0, 0, 0, 0);
+    gather(q0, 0, cwc);
+  }
+  for (uint32_t ch = 0; ch < nch; ++ch) {
+    const uint4 q2 = ch + 2 < nch ? __ldg(src + ch + 2) : q1;
+    uint64_t cwn[4];
+    gather(q1, ch + 1, cwn);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (K == 8 && cwc[u] == ~0ull) continue;
+      const uint32_t lo32 = static_cast<uint32_t>(cwc[u]), hi32 = static_cast<uint32_t>(cwc[u] >> 32);
+#pragma unroll
+      for (int c = 0; c < kChiStride; ++c) {
+        const uint32_t half = c < 4 ? lo32 : hi32;
+        N[c] += nibble_onehot(half, c);
+      }
+    }
+    if (++pend == 3) {
+      flushN();
+      pend = 0;
+      if (++nfl == 20) {
+        flushB();
+        nfl = 0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) cwc[u] = cwn[u];
+    q1 = q2;
+  }
+#else
+  uint4 q = nch ? __ldg(src) : make_uint4(0, 0, 0, 0);
   for (uint32_t ch = 0; ch < nch; ++ch) {
     const uint4 qn = ch + 1 < nch ? __ldg(src + ch + 1) : q;
     const uint32_t ws[4] = {q.x, q.y, q.z, q.w};
@@ -149,6 +198,7 @@ __device__ __forceinline__ void lane_histogram_row(const TriHistArgs& A, uint64_
     }
     q = qn;
   }
+#endif
   flushN();
   flushB();
 }
