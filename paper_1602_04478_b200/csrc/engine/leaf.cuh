@@ -269,13 +269,35 @@ __global__ void __launch_bounds__(256) leaf_hist_kernel(LeafMapArgs A, const uin
     };
     const uint64_t base = A.off[x], end = A.off[x + 1];
     int pend = 0;
-    // 16-byte loads of the row (adj is padded by 16 bytes on upload)
-    for (uint64_t p = base & ~3ull; p < end; p += 4) {
-      const uint4 q = __ldg(reinterpret_cast<const uint4*>(A.adj + p));
-      const uint32_t ws[4] = {q.x, q.y, q.z, q.w};
+    // 16-byte loads of the row (adj is padded by 16 bytes on upload), in a
+    // two-stage pipeline as in the 3-cycle list scan: chunk i+2 and the
+    // colours of chunk i+1 are in flight while chunk i is counted; slots
+    // outside the row count the dummy vertex (colour 7, unused when k < 8)
+    const uint64_t p0 = base & ~3ull;
+    const uint32_t head = static_cast<uint32_t>(base - p0), nn = static_cast<uint32_t>(end - p0);
+    const uint32_t nch = (nn + 3) >> 2;
+    const uint4* src = reinterpret_cast<const uint4*>(A.adj + p0);
+    const bool k8 = A.k >= 8;
+    auto gather = [&](const uint4& qq, uint32_t ch, uint64_t (&cw)[4]) {
+      const uint32_t ws[4] = {qq.x, qq.y, qq.z, qq.w};
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const uint32_t idx = 4 * ch + u;
+        const bool in = idx >= head && idx < nn;
+        cw[u] = k8 ? (in ? load_colors(A.chi, ws[u]) : ~0ull) : load_colors(A.chi, in ? ws[u] : A.nv);
+      }
+    };
+    uint4 q1 = nch > 1 ? __ldg(src + 1) : make_uint4(0, 0, 0, 0);
+    uint64_t cwc[4];
+    gather(nch ? __ldg(src) : make_uint4(0, 0, 0, 0), 0, cwc);
+    for (uint32_t ch = 0; ch < nch; ++ch) {
+      const uint4 q2 = ch + 2 < nch ? __ldg(src + ch + 2) : q1;
+      uint64_t cwn[4];
+      gather(q1, ch + 1, cwn);
       uint64_t cw[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) cw[u] = (p + u >= base && p + u < end) ? load_colors(A.chi, ws[u]) : ~0ull;
+      for (int u = 0; u < 4; ++u) cw[u] = cwc[u], cwc[u] = cwn[u];
+      q1 = q2;
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
         if (cw[u] == ~0ull) continue;
