@@ -461,6 +461,8 @@ __global__ void k_cn_len_keys(const uint64_t* __restrict__ cn_off, uint64_t nout
   const uint64_t len = j < nout ? cn_off[j + 1] - cn_off[j] : 0;
   const unsigned nz = __ballot_sync(0xffffffffu, len > 0);
   if ((threadIdx.x & 31) == 0 && nz) atomicAdd(nonempty, static_cast<u64>(__popc(nz)));
+  const unsigned n2 = __ballot_sync(0xffffffffu, len > 1);  // lists of >= 2 entries: nonempty[1]
+  if ((threadIdx.x & 31) == 0 && n2) atomicAdd(nonempty + 1, static_cast<u64>(__popc(n2)));
   if (j >= nout) return;
   const uint32_t l = static_cast<uint32_t>(len > 0xFFFFFFFFull ? 0xFFFFFFFFull : len);
   if (l) atomicMax(maxlen, l);
