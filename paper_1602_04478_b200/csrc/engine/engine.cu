@@ -279,14 +279,20 @@ __device__ __forceinline__ uint32_t nibble_onehot(uint32_t half, int c) {
   return __funnelshift_l(0u, 1u, sh);
 }
 
-// flag[v] = 1 when v is an endpoint of an oriented edge with a non-empty CN
-// list (a vertex of some triangle).
+// flag1[v] = 1 when v is an endpoint of an oriented edge with a non-empty CN
+// list (a vertex of some triangle), flag2[v] = 1 when of one with >= 2 entries.
 __global__ void k_tri_vertices(uint64_t no, const uint64_t* __restrict__ cn_off, const uint32_t* __restrict__ src,
-                               const uint32_t* __restrict__ nbr, uint8_t* __restrict__ flag) {
+                               const uint32_t* __restrict__ nbr, uint8_t* __restrict__ flag1,
+                               uint8_t* __restrict__ flag2) {
   const uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
-  if (j >= no || cn_off[j + 1] == cn_off[j]) return;
-  flag[src[j]] = 1;
-  flag[nbr[j]] = 1;
+  if (j >= no) return;
+  const uint64_t len = cn_off[j + 1] - cn_off[j];
+  if (len == 0) return;
+  flag1[src[j]] = 1;
+  flag1[nbr[j]] = 1;
+  if (len < 2) return;
+  flag2[src[j]] = 1;
+  flag2[nbr[j]] = 1;
 }
 
 // Edge metadata in list-length order (eorder): meta[i] = (a, b, slot a->b,
