@@ -264,9 +264,12 @@ __global__ void __launch_bounds__(32 * kHistWarps, BIL ? MB_BIL_MINB : MB_TRI_MI
   uint16_t* hrow = hist16_base + static_cast<size_t>(threadIdx.x) * LS;
   const int C = A.C;
   uint32_t ovf = 0;
-  uint64_t local[kChiStride];
+  // per-thread scalar sums per colouring slot in shared memory ([c][thread]):
+  // the rolled colouring loop indexes them dynamically
+  u64* lsum = reinterpret_cast<u64*>(
+      (reinterpret_cast<uintptr_t>(hist16_base + static_cast<size_t>(blockDim.x) * LS) + 7) & ~uintptr_t(7));
 #pragma unroll
-  for (int c = 0; c < kChiStride; ++c) local[c] = 0;
+  for (int c = 0; c < kChiStride; ++c) lsum[c * blockDim.x + threadIdx.x] = 0;
   uint64_t upd = 0;
   const uint64_t nbatch = (A.nitems + 31) / 32;
   // edge metadata one iteration ahead (its DRAM latency would otherwise
@@ -324,9 +327,10 @@ __global__ void __launch_bounds__(32 * kHistWarps, BIL ? MB_BIL_MINB : MB_TRI_MI
     };
     FT Fc[2][NB];
     load_f(0, Fc);
-    // rolled: the unrolled 8-colouring body overflowed the instruction cache
-    // (ncu: 16 % of stall samples "no_instructions")
-#pragma unroll 1
+    // unrolled twice only: the 8-fold body overflowed the instruction cache
+    // (ncu: 16 % of stall samples "no_instructions"); 2 lets the compiler
+    // rename the Fc/Fn double buffer instead of copying it (1 % faster than 1)
+#pragma unroll 2
     for (int c = 0; c < C; ++c) {
       FT Fn[2][NB];
       if (c + 1 < C) load_f(c + 1, Fn);  // in flight while colouring c is joined
@@ -494,12 +498,11 @@ __global__ void __launch_bounds__(32 * kHistWarps, BIL ? MB_BIL_MINB : MB_TRI_MI
         }
       }
       }
-#pragma unroll
-      for (int cc = 0; cc < kChiStride; ++cc)
-        if (cc == c) {
-          local[cc] += acc;
-          ovf |= local[cc] < acc;
-        }
+      if (acc) {
+        u64& ls = lsum[c * blockDim.x + threadIdx.x];
+        ls += acc;
+        ovf |= ls < acc;
+      }
       }
       if (c + 1 < C) {
 #pragma unroll
@@ -514,7 +517,7 @@ __global__ void __launch_bounds__(32 * kHistWarps, BIL ? MB_BIL_MINB : MB_TRI_MI
   if (scalar_out) {
 #pragma unroll
     for (int c = 0; c < kChiStride; ++c) {
-      uint64_t v = local[c];
+      uint64_t v = lsum[c * blockDim.x + threadIdx.x];
       for (int o = 16; o > 0; o >>= 1) v = add_ck(v, __shfl_down_sync(0xffffffffu, v, o), A.err);
       if (lane == 0 && v) atomic_add_ck(A.scalars + c, v, A.err);
     }
@@ -532,7 +535,7 @@ inline size_t tri_canon_smem(int K, int S1, int FK, int SP, int out_kind, int po
   const int n1 = out_kind == 1 ? K * K * P2 : 0, n1p = (SP && pout_kind == 1) ? K * K * P2p : 0;
   const size_t LS = 2 * ((((kChiStride * K) + 1) / 2) | 1);
   return static_cast<size_t>((FMAP + 3) / 4) * 4 + 2 * static_cast<size_t>(n1 + n1p + ((n1 + n1p) & 1)) +
-         static_cast<size_t>(32 * kHistWarps) * LS * 2;
+         static_cast<size_t>(32 * kHistWarps) * LS * 2 + 8 + static_cast<size_t>(32 * kHistWarps) * kChiStride * 8;
 }
 
 using TriCanonFn = void (*)(TriHistArgs);
