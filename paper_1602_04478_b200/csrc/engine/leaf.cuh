@@ -493,7 +493,7 @@ __device__ __forceinline__ void build_pmap(const LeafMapArgs& A, int PB, uint64_
   }
 }
 
-template <int PB, int UNR>
+template <int PB, int UNR, int EB>
 __global__ void __launch_bounds__(256) leaf_pull_kernel(LeafMapArgs A, const uint32_t* __restrict__ vlist,
                                                         uint32_t nv) {
   extern __shared__ u64 lsm[];
@@ -501,7 +501,9 @@ __global__ void __launch_bounds__(256) leaf_pull_kernel(LeafMapArgs A, const uin
   uint32_t* accs = reinterpret_cast<uint32_t*>(lsm + A.k * A.k);
   build_pmap(A, PB, pmap);
   __syncthreads();
-  const uint32_t AS = A.Pout | 1u;
+  // odd stride with at least one spare slot past Pout: map entries that hold
+  // x's colour (slot code 31) land there, so the add loop has no branches
+  const uint32_t AS = (A.Pout + 1) | 1u;
   uint32_t* acc = accs + threadIdx.x * AS;
   const int c = threadIdx.x & 7;
   uint32_t upd = 0;
@@ -533,19 +535,16 @@ __global__ void __launch_bounds__(256) leaf_pull_kernel(LeafMapArgs A, const uin
       for (int u = 0; u < UNR; ++u) {
         cy[u] = ok[u] ? A.chi[static_cast<uint64_t>(y[u]) * kChiStride + c] : cx;
         const uint64_t roff = static_cast<uint64_t>(y[u]) * A.rsb + c * A.psb;
-        if (PB <= 8 && A.ub_e == 2 && A.psb == 8) {
+        if (PB <= 8 && EB == 2 && A.psb == 8) {
           // padded u16 row: one 16-byte load
           const uint4 v4 = ok[u] ? __ldg(reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(A.ub) + roff))
                                  : make_uint4(0, 0, 0, 0);
           const uint32_t wv[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
           for (int e = 0; e < PB; ++e) r[u][e] = (wv[(e >> 1) & 3] >> (16 * (e & 1))) & 0xFFFFu;
-        } else if (A.ub_e == 2) {
-#pragma unroll
-          for (int e = 0; e < PB; ++e) r[u][e] = ok[u] ? ld_entry(A.ub, roff + e, 2) : 0u;
         } else {
 #pragma unroll
-          for (int e = 0; e < PB; ++e) r[u][e] = ok[u] ? ld_entry(A.ub, roff + e, 4) : 0u;
+          for (int e = 0; e < PB; ++e) r[u][e] = ok[u] ? ld_entry(A.ub, roff + e, EB) : 0u;
         }
       }
 #pragma unroll
@@ -554,10 +553,9 @@ __global__ void __launch_bounds__(256) leaf_pull_kernel(LeafMapArgs A, const uin
         const uint64_t w = mx[cy[u]];
 #pragma unroll
         for (int e = 0; e < PB; ++e) {
-          const uint32_t t = static_cast<uint32_t>(w >> (5 * e)) & 31u;
-          if (t == 31u || !r[u][e]) continue;
+          const uint32_t t = min(static_cast<uint32_t>(w >> (5 * e)) & 31u, A.Pout);
           atomicAdd(acc + t, r[u][e]);
-          ++upd;
+          upd += (t < A.Pout) & (r[u][e] != 0);
         }
       }
     }
