@@ -548,9 +548,23 @@ constexpr TriCanonFn canon_ptr() {
   else return nullptr;
 }
 inline TriCanonFn tri_canon_find(int K, int S1, int FK, int SP, bool narrow, bool bil) {
-  if (bil) {  // the config-1 shapes
+  if (bil) {  // the config-1 shapes, and the same two-triangle + pendant-path shape at k = 7
     if (K == 6 && S1 == 5 && FK == 1 && SP == 6 && narrow) return canon_ptr<6, 5, 1, 6, true, true>();
     if (K == 6 && S1 == 5 && FK == 2 && SP == 6 && narrow) return canon_ptr<6, 5, 2, 6, true, true>();
+    // two triangles on the pivot edge with a pendant tree at one pivot end,
+    // fused into the root, at k = 5 and 7 (k - 1 = child size, k = root size)
+    if (K == 5 && S1 == 4 && FK == 1 && SP == 5 && narrow) return canon_ptr<5, 4, 1, 5, true, true>();
+    if (K == 5 && S1 == 4 && FK == 2 && SP == 5 && narrow) return canon_ptr<5, 4, 2, 5, true, true>();
+    if (K == 7 && S1 == 6 && FK == 1 && SP == 7 && narrow) return canon_ptr<7, 6, 1, 7, true, true>();
+    if (K == 7 && S1 == 6 && FK == 2 && SP == 7 && narrow) return canon_ptr<7, 6, 2, 7, true, true>();
+  }
+  // two triangles on one edge (diamond-like fused pairs) and plain triangles
+  // at k = 3, 4, 5, 7
+  if (!narrow && FK == 0 && S1 == 3 && (SP == 0 || SP == 4)) {
+    if (K == 3 && !SP) return canon_ptr<3, 3, 0, 0, false>();
+    if (K == 4) return SP ? canon_ptr<4, 3, 0, 4, false>() : canon_ptr<4, 3, 0, 0, false>();
+    if (K == 5) return SP ? canon_ptr<5, 3, 0, 4, false>() : canon_ptr<5, 3, 0, 0, false>();
+    if (K == 7) return SP ? canon_ptr<7, 3, 0, 4, false>() : canon_ptr<7, 3, 0, 0, false>();
   }
 #define MB_CANON(k_, s_, f_, p_, n_) \
   if (K == k_ && S1 == s_ && FK == f_ && SP == p_ && narrow == n_) return canon_ptr<k_, s_, f_, p_, n_>();
@@ -560,8 +574,8 @@ inline TriCanonFn tri_canon_find(int K, int S1, int FK, int SP, bool narrow, boo
   MB_CANON(k_, 4, 2, 0, true) MB_CANON(k_, 4, 3, 0, false) \
   MB_CANON(k_, 5, 1, 6, false) MB_CANON(k_, 5, 1, 6, true) MB_CANON(k_, 5, 2, 6, false)                   \
   MB_CANON(k_, 5, 2, 6, true)
-  // k = 6 only (the config-1 query and its trees): each instance fully
-  // unrolls the 8-colouring join and costs ~30 s of compile time; other k use
+  // the full shape list for k = 6 (the config-1 query and its trees) only:
+  // each instance costs seconds of compile time; other shapes use
   // tri_hist_kernel
   MB_CANON_K(6)
 #undef MB_CANON_K
