@@ -16,8 +16,17 @@
 // compile-time constants and every product is a register multiply-add.  Only
 // three things still depend on the lane's colours: which histogram counts
 // form h (R[r] = r-th colour not in {c0, c1}), where a node factor keyed by one
-// pivot colour keeps its R-entries (a per-CTA byte map over (c_f, c_other)),
-// and the index of a unary output entry (the existing idx1 maps).
+// pivot colour keeps its R-entries (a per-CTA map over (c_f, c_other), 4 bits
+// per entry packed in one word), and the index of a unary output entry (the
+// idx1 maps).  A fused child + parent collapses into one bilinear form in h
+// (see the BIL path below).
+//
+// Per edge: metadata and list range are read coalesced (permuted into the
+// list-length order at prep) one iteration ahead; the list scan is a
+// two-stage pipeline (lane_histogram_row); the colouring loop is unrolled
+// twice only (instruction cache) with the factor gathers one colouring ahead.
+// MB_TRI_DEBUG (timing split only; counts are wrong): 1 skips the join, 2
+// the scan, 4 the factor gathers.
 //
 // Reference semantics: the same 3-cycle block evaluation by DB as
 // tri_hist_kernel (engine.cpp:353-366, table.cpp:255-476 for the joins).
