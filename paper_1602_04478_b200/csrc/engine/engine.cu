@@ -462,7 +462,7 @@ unsigned grid_for(uint64_t work, unsigned block) {
 // source vertex, so lanes of a warp share sources and their factor rows.
 __global__ void k_cn_len_keys(const uint64_t* __restrict__ cn_off, uint64_t nout, uint64_t* __restrict__ keys,
                               uint32_t* __restrict__ vals, u64* __restrict__ nonempty,
-                              unsigned* __restrict__ maxlen) {
+                              unsigned* __restrict__ maxlen, uint32_t fmask /* fraction bits */) {
   const uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   const uint64_t len = j < nout ? cn_off[j + 1] - cn_off[j] : 0;
   const unsigned nz = __ballot_sync(0xffffffffu, len > 0);
@@ -474,11 +474,13 @@ __global__ void k_cn_len_keys(const uint64_t* __restrict__ cn_off, uint64_t nout
   if (l) atomicMax(maxlen, l);
   uint32_t bucket = 0;  // 0 for empty lists: sorted last
   if (l) {
-    const uint32_t b = 31 - __clz(l);
-    const uint32_t frac = b >= 2 ? (l >> (b - 2)) & 3u : (l << (2 - b)) & 3u;
-    bucket = 1 + 4 * b + frac;
+    // fmask = number of fraction bits F: 2^F buckets per octave
+    const uint32_t b = 31 - __clz(l), F = fmask;
+    const uint32_t frac = b >= F ? (l >> (b - F)) & ((1u << F) - 1u) : (l << (F - b)) & ((1u << F) - 1u);
+    bucket = 1 + (b << F) + frac;
+    if (l == 1) bucket = 1;  // one-entry lists stay the last non-empty bucket
   }
-  keys[j] = (static_cast<uint64_t>(0xFFu - bucket) << 32) | static_cast<uint32_t>(j);
+  keys[j] = (static_cast<uint64_t>(0xFFFFu - bucket) << 32) | static_cast<uint32_t>(j);
   vals[j] = static_cast<uint32_t>(j);
 }
 
