@@ -507,7 +507,8 @@ __global__ void __launch_bounds__(256) leaf_pull_kernel(LeafMapArgs A, const uin
   uint32_t* acc = accs + threadIdx.x * AS;
   const int c = threadIdx.x & 7;
   uint32_t upd = 0;
-  for (uint32_t gi = blockIdx.x * 32 + (threadIdx.x >> 3); gi < nv; gi += gridDim.x * 32) {
+  const uint32_t gpc = blockDim.x >> 3;  // vertex groups (of 8 slots) per CTA
+  for (uint32_t gi = blockIdx.x * gpc + (threadIdx.x >> 3); gi < nv; gi += gridDim.x * gpc) {
     if (c >= A.C) continue;
     const uint32_t x = vlist[gi];
     for (uint32_t i = 0; i < A.Pout; ++i) acc[i] = 0;
