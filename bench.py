@@ -46,13 +46,13 @@ CONFIGS = {
             query=[(0, 1), (1, 2), (2, 0), (1, 3), (3, 2), (2, 4), (4, 5)], seeds=list(range(100, 108)),
             sample_n=20_000),
     2: dict(name="rmat22_c7", gen=("rmat", 22, 16, 3), k=7, query=[(i, (i + 1) % 7) for i in range(7)],
-            seeds=list(range(200, 216)), sample_n=10),  # sample: R-MAT scale 10
+            seeds=list(range(200, 216)), sample_n=10, overflows=True),  # sample: R-MAT scale 10
     3: dict(name="chunglu4m_theta8", gen=("cl", 4_000_000, 2.3, 20.0, 4), k=8,
             query=[(0, 1), (1, 2), (2, 7), (0, 3), (3, 4), (4, 7), (0, 5), (5, 6), (6, 7)],
             seeds=list(range(300, 316)), sample_n=500),
     4: dict(name="chunglu2m_sp10", gen=("cl", 2_000_000, 2.1, 24.0, 5), k=10,
             query=[(0, 1), (1, 2), (2, 3), (3, 4), (4, 5), (5, 0), (0, 2), (3, 5), (1, 6), (6, 7), (7, 8),
-                   (8, 9), (9, 1)], seeds=list(range(400, 464)), sample_n=600),
+                   (8, 9), (9, 1), (1, 8)], seeds=list(range(400, 464)), sample_n=600, overflows=True),
 }
 
 
@@ -170,62 +170,169 @@ def ref_layout(nc):
     return threads, max(1, ncpu // threads)
 
 
-def reference_arm(args, cfg, ws, rank):
-    if rank != 0:
-        return
+def sample_edges(cfg, n_override):
+    """Edge list of the workload's bounded sample, generated by the product's
+    seeded generator in a CHILD process and handed over as a .npy file, so the
+    process that times the reference never maps libmotif_b200.so."""
+    import tempfile
+
+    gen = cfg["gen"]
+    tag = "_".join(str(x) for x in gen) + f"_{n_override}"
+    path = os.path.join(tempfile.gettempdir(), f"mb_sample_{tag}.npz")
+    if not os.path.exists(path):
+        code = ("import sys, numpy as np; sys.path.insert(0, %r)\n"
+                "import paper_1602_04478_b200 as mb\n"
+                "from bench import CONFIGS, make_graph\n"
+                "g = make_graph(mb, CONFIGS[%d]['gen'], %r)\n"
+                "np.savez(%r, n=g.num_vertices(), edges=g.edges())\n") % (ROOT, cfg["id"], n_override, path)
+        subprocess.run([sys.executable, "-c", code], check=True)
+    d = np.load(path)
+    return int(d["n"]), d["edges"]
+
+
+def time_reference(cfg, n_override, steps=1, warmup=0):
+    """The compiled reference (oracle/_ref, DB engine, OpenMP) on the sample:
+    one colouring per host thread, spare cores as BSP workers."""
     from oracle import Reference
 
-    import paper_1602_04478_b200 as mb
-
-    n_sample = cfg["sample_n"] or 10_000
-    g = make_graph(mb, cfg["gen"], n_sample)
+    n, edges = sample_edges(cfg, n_override)
     R = Reference()
-    rg = R.graph(g.num_vertices(), g.edges())
+    rg = R.graph(n, edges)
     rp = R.plan(cfg["k"], cfg["query"])
     seeds = cfg["seeds"][:16]  # bounded sample: at most 16 colourings per step (one per host core)
     chis = np.stack([rg.coloring(cfg["k"], s) for s in seeds])
     threads, workers = ref_layout(len(chis))
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         R.count_batch(rg, rp, chis[: min(len(chis), threads)], engine=1, threads=threads, workers=workers)
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        R.count_batch(rg, rp, chis, engine=1, threads=threads, workers=workers)
-    dt = (time.perf_counter() - t0) / args.steps
-    v = len(seeds) / dt
-    sample = (f"{cfg['name']} generator at n={g.num_vertices()} (m={g.num_edges()}), same query/k/seeds; "
-              f"{len(seeds)} colourings per step, {threads} at a time x {workers} BSP workers each")
+    for _ in range(steps):
+        counts = R.count_batch(rg, rp, chis, engine=1, threads=threads, workers=workers)
+    dt = (time.perf_counter() - t0) / steps
+    return {"value": len(seeds) / dt, "dt": dt, "n": n, "m": len(edges), "colorings": len(seeds), "threads": threads,
+            "workers": workers, "counts": [int(c) for c in counts], "seeds": seeds}
+
+
+def reference_arm(args, cfg, ws, rank):
+    if rank != 0:
+        return
+    r = time_reference(cfg, cfg["sample_n"], args.steps, args.warmup)
+    v = r["value"]
+    sample = (f"{cfg['name']} generator at n={r['n']} (m={r['m']}), same query/k/seeds; {r['colorings']} colourings "
+              f"per step, {r['threads']} at a time x {r['workers']} BSP workers each")
     print(json.dumps({
         "impl": "reference", "metric": "colorings/sec", "value": v, "unit": "colorings/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": r["dt"] * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
-        "config": {"workload": cfg["name"], "sample_n": g.num_vertices(), "colorings_per_step": len(seeds)},
-        "cpu_baseline": {"value": v, "unit": "colorings/s", "cores": threads * workers,
+        "config": {"workload": cfg["name"], "sample_n": r["n"], "colorings_per_step": r["colorings"]},
+        "cpu_baseline": {"value": v, "unit": "colorings/s", "cores": r["threads"] * r["workers"],
                          "kind": "reference", "sample": sample},
         "e2e": {"value": v, "unit": "colorings/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "counts_first3": r["counts"][:3],
     }), flush=True)
 
 
 def cpu_baseline(cfg):
-    from oracle import Reference, reference_available
-
-    import paper_1602_04478_b200 as mb
+    from oracle import reference_available
 
     if not reference_available() or not cfg["sample_n"]:
         return None
-    g = make_graph(mb, cfg["gen"], cfg["sample_n"])
-    R = Reference()
-    rg = R.graph(g.num_vertices(), g.edges())
-    rp = R.plan(cfg["k"], cfg["query"])
-    chis = np.stack([rg.coloring(cfg["k"], s) for s in cfg["seeds"][:16]])
-    threads, workers = ref_layout(len(chis))
-    t0 = time.perf_counter()
-    R.count_batch(rg, rp, chis, engine=1, threads=threads, workers=workers)
-    dt = time.perf_counter() - t0
-    return {"value": len(chis) / dt, "unit": "colorings/s", "cores": threads * workers,
-            "kind": "reference",
+    r = time_reference(cfg, cfg["sample_n"])
+    return {"value": r["value"], "unit": "colorings/s", "cores": r["threads"] * r["workers"], "kind": "reference",
+            "counts": r["counts"],
             "sample": (f"compiled reference (oracle/_ref, DB engine) on the {cfg['name']} generator at "
-                       f"n={g.num_vertices()} (m={g.num_edges()}): {len(chis)} colourings in {dt:.1f}s, "
-                       f"{threads} colourings at a time x {workers} BSP workers each")}
+                       f"n={r['n']} (m={r['m']}): {r['colorings']} colourings in {r['dt']:.1f}s, "
+                       f"{r['threads']} colourings at a time x {r['workers']} BSP workers each")}
+
+
+def gpu_rate(mb, g, plan, nb, chis_dev, pinned, steps, warmup, flush, dev):
+    """Device-timed (CUDA events on the engine stream, L2 flushed between
+    steps) and end-to-end (public C ABI, pinned host colourings, copies inside
+    the region) colourings/s of one graph; returns counts too."""
+    import torch
+
+    stream = torch.cuda.ExternalStream(mb.engine_stream(g), device=dev)
+    for _ in range(max(warmup, 0)):
+        mb.count_colorful_device(g, plan, chis_dev.data_ptr(), nb)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    torch.cuda.synchronize()
+    for i in range(steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        starts[i].record(stream)
+        counts = mb.count_colorful_device(g, plan, chis_dev.data_ptr(), nb)
+        ends[i].record(stream)
+    torch.cuda.synchronize()
+    ms = float(np.mean([a.elapsed_time(b) for a, b in zip(starts, ends)]))
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        c = mb.count_colorful(g, plan, pinned.numpy())
+    e2e_s = (time.perf_counter() - t0) / steps
+    assert np.array_equal(c, counts)
+    return ms, e2e_s, counts
+
+
+def overflow_arm(args, cfg, ws, rank, local, g, plan, dev):
+    """A workload whose colourful count is >= 2^64: the reference's checked
+    u64 arithmetic raises OverflowError (errors.hpp:38-50), and so does the
+    engine, failing fast at the first overflowing add.  A step resolves
+    `per_step` colourings (one call each, as each would end the reference's
+    estimate()); value = colourings resolved per second."""
+    import torch
+
+    import paper_1602_04478_b200 as mb
+
+    k, n = cfg["k"], g.num_vertices()
+    per_step = min(len(cfg["seeds"]), args.overflow_colorings)
+    seeds = [s + rank * 1000 for s in cfg["seeds"][:per_step]]
+    chis = [mb.random_coloring(g, k, s) for s in seeds]
+    outcomes = []
+
+    def step():
+        res = []
+        for chi in chis:
+            try:
+                res.append(int(mb.count_colorful(g, plan, chi)))
+            except mb.CountOverflowError:
+                res.append("OverflowError")
+        return res
+
+    t0 = time.perf_counter()
+    outcomes = step()  # first call: upload + indexes
+    first_call_s = time.perf_counter() - t0
+    for _ in range(max(args.warmup - 1, 0)):
+        step()
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        res = step()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / max(args.steps, 1)
+    clk = clocks.stop()
+    t = torch.tensor([dt], dtype=torch.float64, device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    dt = float(t.item())
+    assert res == outcomes
+    line = {
+        "metric": "colorings/sec", "value": per_step * ws / dt, "unit": "colorings/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": cfg["name"] + (f"@size{args.size}" if args.size else ""), "n": n,
+                   "m": g.num_edges(), "k": k, "colorings_per_step": per_step, "query_edges": cfg["query"],
+                   "first_call_s": first_call_s,
+                   "timing": "host wall clock around whole calls (each ends in an exception)"},
+        "outcome": outcomes,
+        "e2e": {"value": per_step * ws / dt, "unit": "colorings/s", "h2d_bytes_per_step": int(per_step * n),
+                "d2h_bytes_per_step": int(8 * per_step)},
+        "gpu_launches": None, "clocks": clk,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
 
 
 def our_arm(args, cfg, ws, rank, local):
@@ -238,6 +345,8 @@ def our_arm(args, cfg, ws, rank, local):
     g = make_graph(mb, cfg["gen"], args.size)
     plan = mb.QueryPlan(cfg["k"], cfg["query"])
     k, n = cfg["k"], g.num_vertices()
+    if cfg.get("overflows") and not args.size:
+        return overflow_arm(args, cfg, ws, rank, local, g, plan, dev)
     # weak scaling: rank r counts its own batch (seed offset r * batch)
     nb = len(cfg["seeds"])
     seeds = [s + rank * 1000 for s in cfg["seeds"]]
@@ -246,11 +355,13 @@ def our_arm(args, cfg, ws, rank, local):
     pinned = torch.from_numpy(chis_host).pin_memory()
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
-    # first call uploads the graph and builds the plan-derived indexes
+    # first call: graph upload + plan-derived indexes + the count, from host
+    # colourings (the cold end-to-end figure)
     t0 = time.perf_counter()
-    counts0 = mb.count_colorful_device(g, plan, chis_dev.data_ptr(), nb)
+    counts0 = mb.count_colorful(g, plan, pinned.numpy())
     first_call_s = time.perf_counter() - t0
     prep_ms = mb.engine_prep_ms(g)
+    assert mb.engine_device(g) == local, "engine not on this rank's device"
     stream = torch.cuda.ExternalStream(mb.engine_stream(g), device=dev)
 
     def step():
@@ -325,6 +436,9 @@ def our_arm(args, cfg, ws, rank, local):
                    "graph_prep_ms": prep_ms, "first_call_s": first_call_s},
         "e2e": {"value": e2e_value, "unit": "colorings/s", "h2d_bytes_per_step": int(nb * n),
                 "d2h_bytes_per_step": int(8 * nb + 24 * nb)},
+        # cold end to end: a fresh graph handle's first call (graph upload,
+        # degree-ordered relabel, common-neighbour index, the count)
+        "e2e_cold": {"value": nb / first_call_s, "unit": "colorings/s", "seconds": first_call_s},
         "gpu_launches": int(launches),
         "roofline": {"bound": "hbm", "kernel": top[0], "achieved": achieved, "peak": peaks["hbm_gbs"],
                      "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": committed_traffic(top[0]),
@@ -336,8 +450,27 @@ def our_arm(args, cfg, ws, rank, local):
         "clocks": clk,
         "counts_first3": [int(x) for x in counts0[:3]],
     }
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(cfg)
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline and not args.size:
+        cpu = cpu_baseline(cfg)
+        line["cpu_baseline"] = cpu
+        if cpu:
+            # same input for both: the GPU on the reference's bounded sample
+            gs = make_graph(mb, cfg["gen"], cfg["sample_n"])
+            ss = cfg["seeds"][:16]
+            cs = np.stack([mb.random_coloring(gs, k, s) for s in ss])
+            cs_dev = torch.from_numpy(cs).to(dev)
+            cs_pin = torch.from_numpy(cs).pin_memory()
+            sms, se2e, scounts = gpu_rate(mb, gs, plan, len(ss), cs_dev, cs_pin, max(args.steps, 3), 2, flush, dev)
+            same = [int(x) for x in scounts] == cpu["counts"]
+            line["same_input"] = {
+                "n": gs.num_vertices(), "m": gs.num_edges(), "colorings": len(ss),
+                "value": len(ss) / (sms / 1e3), "e2e": len(ss) / se2e, "reference_value": cpu["value"],
+                "ratio": len(ss) / (sms / 1e3) / cpu["value"], "e2e_ratio": len(ss) / se2e / cpu["value"],
+                "counts_equal_reference": same, "same_config": True}
+            if not same:
+                raise SystemExit("bench: GPU counts differ from the reference on the same input")
+        if cpu:
+            cpu.pop("counts", None)
     if rank == 0:
         print(json.dumps(line), flush=True)
 
@@ -350,11 +483,13 @@ def main():
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--overflow-colorings", type=int, default=4,
+                    help="colourings resolved per step on workloads whose count overflows u64 (configs 2, 4)")
     ap.add_argument("--size", type=int, default=None,
                     help="override the generator size (n, or the R-MAT scale): supplementary reduced runs of "
                          "configs 2-4, whose full sizes exceed u64 counts or HBM (DESIGN.md)")
     args = ap.parse_args()
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config], id=args.config)
     ws, rank, local = dist_setup(args)
     try:
         if args.impl == "reference":

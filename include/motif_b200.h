@@ -112,6 +112,12 @@ double mb_coefficient_of_variation(const uint64_t* counts, uint64_t n);
 int mb_estimate(mb_graph* g, mb_plan* p, int engine, uint64_t trials, uint64_t seed,
                 uint64_t* per_trial, double* mean, double* cv, uint64_t* aut, double* subgraph);
 
+/* The report of estimate() from per-trial colourful counts gathered elsewhere
+ * (the sharded multi-rank estimate): norm * mean in long double exactly as
+ * estimate.cpp:124-127, cv, and mean / aut. */
+int mb_estimate_from_counts(int k, uint64_t aut, const uint64_t* per_trial, uint64_t trials,
+                            double* mean, double* cv, double* subgraph);
+
 /* ---- 1-D partition (include/motif/runtime.hpp:14-36) ----------------------- */
 
 /* Partition(n, p): block_begin / block_size / owner; returns 8 if p<1 or p>n. */
@@ -125,8 +131,14 @@ int mb_engine_enable_timing(mb_graph* g, int on);
  * (summed) and name of entry idx; returns 8 when idx is past the end. */
 int mb_engine_kernel_timing(mb_graph* g, int idx, char* name, int len, double* ms,
                             uint64_t* launches, uint64_t* bytes);
-/* cudaStream_t the engine launches on (for CUDA-event timing by callers). */
+/* cudaStream_t the engine launches on (for CUDA-event timing by callers).
+ * mb_count_colorful_device reads chi_dev on this stream: a caller that fills
+ * chi_dev on another stream must synchronise that stream first. */
 void* mb_engine_stream(mb_graph* g);
+/* CUDA device of the graph's engine (-1 before the first count).  The engine
+ * is created on the caller's current device at the first counting call and
+ * every later call runs there, restoring the caller's current device. */
+int mb_engine_device(const mb_graph* g);
 /* Milliseconds spent building plan-derived graph indexes (triangle lists). */
 double mb_engine_prep_ms(mb_graph* g);
 uint64_t mb_engine_launches(mb_graph* g);

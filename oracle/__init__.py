@@ -60,6 +60,8 @@ class Oracle:
         L.or_normalization_factor.argtypes = [C.c_int]
         L.or_coefficient_of_variation.restype = C.c_double
         L.or_coefficient_of_variation.argtypes = [u64p, C.c_uint64]
+        L.or_q6_colorful.restype = C.c_int
+        L.or_q6_colorful.argtypes = [C.c_uint32, u64p, u32p, C.c_int, u8p, u64p]
         self.L = L
 
     def mt64(self, seed: int, count: int) -> np.ndarray:
@@ -102,6 +104,21 @@ class Oracle:
         if rc:
             raise OracleError(rc, "oracle budget exceeded")
         return out.value
+
+    def q6_colorful(self, off, adj, chis) -> list:
+        """Independent OpenMP counter of BASELINE config 1's query (q6_count.c)
+        for a batch of colourings (c, n); raises on u64 overflow."""
+        off = np.ascontiguousarray(off, dtype=np.uint64)
+        adj = np.ascontiguousarray(adj, dtype=np.uint32)
+        chis = np.ascontiguousarray(np.atleast_2d(chis), dtype=np.uint8)
+        out = np.zeros(chis.shape[0], dtype=np.uint64)
+        rc = self.L.or_q6_colorful(len(off) - 1, _p(off, C.c_uint64), _p(adj, C.c_uint32), chis.shape[0],
+                                   _p(chis, C.c_uint8), _p(out, C.c_uint64))
+        if rc == -1:
+            raise OracleError(4, "count overflow (64-bit)")
+        if rc != 0:
+            raise OracleError(8, f"q6 counter failed ({rc})")
+        return [int(x) for x in out]
 
     def automorphism_count(self, k, qedges) -> int:
         q = np.ascontiguousarray(np.asarray(qedges, dtype=np.int32).reshape(-1, 2))

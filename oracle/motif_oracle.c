@@ -4,15 +4,15 @@
  *
  * A plain-C restatement of the reference's ground-truth path (arXiv 1602.04478
  * artifact, /root/reference/proj):
- *   - splitmix64 / derive_seed / uniform_below ...... include/motif/rng.hpp:96-118
+ *   - splitmix64 / derive_seed / uniform_below ...... include/motif/rng.hpp:9-31
  *   - mt19937_64 (std::mt19937_64, the reference's engine; standard MT19937-64)
- *   - random_coloring ............................... src/graph.cpp:328-337
- *   - DataGraph::from_edges normalisation ........... src/graph.cpp:200-230
- *   - degree_rank ................................... src/graph.cpp:309-320
- *   - brute_matches / brute_colorful backtracker .... src/oracle.cpp:223-317
- *   - automorphism_count ............................ src/estimate.cpp:57-86
- *   - normalization_factor (k^k/k!) ................. src/estimate.cpp:88-120
- *   - coefficient_of_variation ...................... src/estimate.cpp:122-135
+ *   - random_coloring ............................... src/graph.cpp:142-151
+ *   - DataGraph::from_edges normalisation ........... src/graph.cpp:14-44
+ *   - degree_rank ................................... src/graph.cpp:123-134
+ *   - brute_matches / brute_colorful backtracker .... src/oracle.cpp:11-105
+ *   - automorphism_count ............................ src/estimate.cpp:14-45
+ *   - normalization_factor (k^k/k!) ................. src/estimate.cpp:47-79
+ *   - coefficient_of_variation ...................... src/estimate.cpp:81-94
  *
  * Pinned by tests/test_oracle.py against (a) the known answers in the
  * reference's own tests (tests/test_oracle.cpp, test_engine.cpp, test_graph.cpp,

@@ -43,7 +43,7 @@ __all__ = [
     "SchemaError", "ContractError", "SpecError", "CudaError",
     "DataGraph", "QueryPlan", "EstimateReport", "Partition", "load_edge_list", "degree_rank",
     "random_coloring", "derive_seed", "count_colorful", "estimate", "automorphism_count",
-    "normalization_factor", "coefficient_of_variation", "PS", "DB", "lib",
+    "normalization_factor", "coefficient_of_variation", "estimate_from_counts", "PS", "DB", "lib",
 ]
 
 PS, DB = 0, 1
@@ -132,6 +132,8 @@ def _load() -> C.CDLL:
         "mb_automorphism_count": (C.c_int, [C.c_int, i32p, C.c_int, u64p]),
         "mb_normalization_factor": (C.c_double, [C.c_int]),
         "mb_coefficient_of_variation": (C.c_double, [u64p, C.c_uint64]),
+        "mb_estimate_from_counts": (C.c_int, [C.c_int, C.c_uint64, u64p, C.c_uint64, C.POINTER(C.c_double),
+                                              C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "mb_estimate": (C.c_int, [P, P, C.c_int, C.c_uint64, C.c_uint64, u64p, C.POINTER(C.c_double),
                                   C.POINTER(C.c_double), u64p, C.POINTER(C.c_double)]),
         "mb_partition_block": (C.c_int, [C.c_uint32, C.c_int, C.c_int, u32p, u32p]),
@@ -140,6 +142,7 @@ def _load() -> C.CDLL:
         "mb_engine_kernel_timing": (C.c_int, [P, C.c_int, C.c_char_p, C.c_int, C.POINTER(C.c_double), u64p,
                                               u64p]),
         "mb_engine_stream": (C.c_void_p, [P]),
+        "mb_engine_device": (C.c_int, [P]),
         "mb_engine_prep_ms": (C.c_double, [P]),
         "mb_engine_launches": (C.c_uint64, [P]),
         "mb_engine_stats": (C.c_int, [P, u64p, u64p, u64p]),
@@ -392,6 +395,21 @@ def estimate(g: DataGraph, plan: QueryPlan, engine: int, trials: int, seed: int)
                           cv.value, aut.value, sub.value)
 
 
+def estimate_from_counts(k: int, edges, per_trial) -> EstimateReport:
+    """estimate()'s report (estimate.cpp:124-129) from per-trial colourful
+    counts computed elsewhere (the sharded multi-rank estimate): the mean is
+    taken in long double by the library, as the reference does."""
+    per = np.ascontiguousarray(per_trial, dtype=np.uint64)
+    if len(per) < 1:
+        raise SpecError("trials must be >= 1")
+    aut = automorphism_count(k, edges)
+    mean, cv, sub = C.c_double(), C.c_double(), C.c_double()
+    _check(lib.mb_estimate_from_counts(k, aut, _ptr(per, C.c_uint64), len(per), C.byref(mean), C.byref(cv),
+                                       C.byref(sub)))
+    return EstimateReport(len(per), [int(x) for x in per], normalization_factor(k), mean.value, cv.value, aut,
+                          sub.value)
+
+
 class Partition:
     """1-D block distribution of vertices over p workers (runtime.hpp:14)."""
 
@@ -435,6 +453,11 @@ def engine_timings(g: DataGraph) -> list[tuple[str, float, int, int]]:
 
 def engine_enable_timing(g: DataGraph, on: bool = True) -> None:
     _check(lib.mb_engine_enable_timing(g.handle, 1 if on else 0))
+
+
+def engine_device(g: DataGraph) -> int:
+    """CUDA device the graph's engine runs on (-1 before the first count)."""
+    return lib.mb_engine_device(g.handle)
 
 
 def engine_stream(g: DataGraph) -> int:

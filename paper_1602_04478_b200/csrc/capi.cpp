@@ -52,7 +52,9 @@ int guarded(F&& f) {
 
 mb::GpuEngine& engine_for(mb_graph* g, mb_plan* p) {
   if (!g->eng) {
-    g->eng = std::make_unique<mb::GpuEngine>(g->g, 0);
+    // created on the caller's current device (torch.cuda.set_device(local_rank)
+    // under torchrun); every later call runs there and restores the caller's
+    g->eng = std::make_unique<mb::GpuEngine>(g->g, -1);
     g->eng->enable_timing(g->timing);
     g->bound = nullptr;
   }
@@ -229,16 +231,29 @@ int mb_count_colorful_seeds(mb_graph* g, mb_plan* p, const uint64_t* seeds, int 
                             uint64_t* out) {
   return guarded([&] {
     if (engine != 0 && engine != 1) mb::fail(mb::kSpec, "engine must be 0 (PS) or 1 (DB)");
+    if (ncol < 0) mb::fail(mb::kSpec, "negative colouring count");
+    auto& eng = engine_for(g, p);
     const uint32_t n = g->g.n;
-    std::vector<uint8_t> chi(static_cast<size_t>(n) * ncol);
-    std::vector<std::thread> ts;
-    for (int c = 0; c < ncol; ++c)
-      ts.emplace_back([&, c] {
-        const auto col = mb::random_coloring(n, p->q.k, seeds[c]);
-        std::memcpy(chi.data() + static_cast<size_t>(c) * n, col.data(), n);
-      });
-    for (auto& t : ts) t.join();
-    engine_for(g, p).count(chi.data(), ncol, true, out);
+    // bounded batches (as mb_estimate): at most 64 colourings or 256 MB of
+    // host colours per device call, generated by a fixed pool of threads
+    const int batch = static_cast<int>(
+        std::max<uint64_t>(1, std::min<uint64_t>(64, (256ull << 20) / std::max<uint32_t>(n, 1))));
+    const int nthreads = static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
+    std::vector<uint8_t> chi;
+    for (int c0 = 0; c0 < ncol; c0 += batch) {
+      const int nb = std::min(batch, ncol - c0);
+      chi.resize(static_cast<size_t>(n) * nb);
+      std::vector<std::thread> ts;
+      for (int t = 0; t < std::min(nthreads, nb); ++t)
+        ts.emplace_back([&, t] {
+          for (int c = t; c < nb; c += nthreads) {
+            const auto col = mb::random_coloring(n, p->q.k, seeds[c0 + c]);
+            std::memcpy(chi.data() + static_cast<size_t>(c) * n, col.data(), n);
+          }
+        });
+      for (auto& t : ts) t.join();
+      eng.count(chi.data(), nb, true, out + c0);
+    }
   });
 }
 
@@ -261,6 +276,19 @@ double mb_normalization_factor(int k) {
     g_err = e.what();
     return 0.0;
   }
+}
+
+int mb_estimate_from_counts(int k, uint64_t aut, const uint64_t* per_trial, uint64_t trials, double* mean,
+                            double* cv, double* subgraph) {
+  return guarded([&] {
+    if (trials < 1) mb::fail(mb::kSpec, "trials must be >= 1");
+    const double norm = mb::normalization_factor(k);
+    long double sum = 0;
+    for (uint64_t i = 0; i < trials; ++i) sum += static_cast<long double>(per_trial[i]);
+    *mean = static_cast<double>(norm * (sum / static_cast<long double>(trials)));
+    *cv = mb::coefficient_of_variation(std::vector<uint64_t>(per_trial, per_trial + trials));
+    *subgraph = *mean / static_cast<double>(aut);
+  });
 }
 
 double mb_coefficient_of_variation(const uint64_t* counts, uint64_t n) {
@@ -288,12 +316,10 @@ int mb_estimate(mb_graph* g, mb_plan* p, int engine, uint64_t trials, uint64_t s
       }
       eng.count(chi.data(), static_cast<int>(nb), true, per_trial + t0);
     }
-    long double sum = 0;
-    for (uint64_t i = 0; i < trials; ++i) sum += static_cast<long double>(per_trial[i]);
-    *mean = static_cast<double>(norm * (sum / static_cast<long double>(trials)));
-    *cv = mb::coefficient_of_variation(std::vector<uint64_t>(per_trial, per_trial + trials));
+    (void)norm;
     *aut = mb::automorphism_count(p->q);
-    *subgraph = *mean / static_cast<double>(*aut);
+    const int rc = mb_estimate_from_counts(p->q.k, *aut, per_trial, trials, mean, cv, subgraph);
+    if (rc) mb::fail(static_cast<mb::Status>(rc), g_err);
   });
 }
 
@@ -341,6 +367,8 @@ int mb_engine_kernel_timing(mb_graph* g, int idx, char* name, int len, double* m
 }
 
 void* mb_engine_stream(mb_graph* g) { return g->eng ? g->eng->stream() : nullptr; }
+
+int mb_engine_device(const mb_graph* g) { return g->eng ? g->eng->device() : -1; }
 
 double mb_engine_prep_ms(mb_graph* g) { return g->eng ? g->eng->stats().prep_ms : 0.0; }
 

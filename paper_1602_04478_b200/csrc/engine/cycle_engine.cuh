@@ -83,11 +83,56 @@ struct HopArgs {
   uint32_t P_out;
   int out_has_r;
   int bits;
-  uint64_t* key_out;     // [W]
-  uint64_t* row_out;     // [W][P_out]
+  uint64_t* key_out;     // [distinct keys] (keys pass)
+  uint64_t* row_out;     // [distinct keys][P_out] (accumulate pass)
+  // open-addressing hash table of the output keys: slot -> dense index
+  uint64_t* ht_key;
+  uint32_t* ht_idx;
+  uint64_t ht_mask;
+  int ht_shift;
+  unsigned long long* n_keys;
   int* err;
   u64* updates;
 };
+
+constexpr uint64_t kEmptyKey = ~0ull;
+
+__device__ __forceinline__ uint64_t ht_slot(uint64_t key, int shift) {
+  return (key * 0x9E3779B97F4A7C15ull) >> shift;
+}
+
+// Inserts `key` (keys pass): the first inserter takes the next dense index.
+__device__ __forceinline__ void ht_insert(uint64_t* ht_key, uint32_t* ht_idx, uint64_t mask, int shift, uint64_t key,
+                                          unsigned long long* n_keys, uint64_t* key_out) {
+  uint64_t h = ht_slot(key, shift);
+  while (true) {
+    const uint64_t cur = ht_key[h];
+    if (cur == key) return;
+    if (cur == kEmptyKey) {
+      const uint64_t prev = atomicCAS(reinterpret_cast<unsigned long long*>(ht_key + h), kEmptyKey, key);
+      if (prev == kEmptyKey) {
+        const uint32_t idx = static_cast<uint32_t>(atomicAdd(n_keys, 1ull));
+        ht_idx[h] = idx;
+        key_out[idx] = key;
+        return;
+      }
+      if (prev == key) return;
+    }
+    h = (h + 1) & mask;
+  }
+}
+
+// Dense index of a key known to be present (after the keys pass), or ~0u.
+__device__ __forceinline__ uint32_t ht_find(const uint64_t* __restrict__ ht_key, const uint32_t* __restrict__ ht_idx,
+                                            uint64_t mask, int shift, uint64_t key) {
+  uint64_t h = ht_slot(key, shift);
+  while (true) {
+    const uint64_t cur = ht_key[h];
+    if (cur == key) return ht_idx[h];
+    if (cur == kEmptyKey) return ~0u;
+    h = (h + 1) & mask;
+  }
+}
 
 __device__ __forceinline__ uint64_t pack_key(uint64_t x, uint64_t v, uint64_t r, int has_r, int bits) {
   return has_r ? (((x << bits) | v) << bits) | r : (x << bits) | v;
@@ -133,10 +178,15 @@ __global__ void k_hop_work(const uint64_t* __restrict__ key_in, uint64_t n_in, i
 
 constexpr int kHopTile = 256;  // items per CTA of k_hop_expand
 
-// One thread per (frontier entry, neighbour) work item; writes the item's key
-// (UINT64_MAX when it contributes nothing) and its dense colour-set row.  The
-// CTA locates its items' entries once: the woff span of its tile is staged in
-// shared memory and each thread searches there.
+// One thread per (frontier entry, neighbour) work item, two passes over the
+// same items.  KEYS: the item's output key (x, w[, r]) is inserted into an
+// open-addressing hash table that hands out dense indices.  ACCUMULATE: the
+// item's contributions are added straight into the dense row of its key.
+// This replaces the reference's hash-map accumulate (table.cpp:38-54) without
+// materialising a row per item or sorting: aggregation costs one probe plus
+// the row atomics of the nonzero contributions.  The CTA locates its items'
+// entries once: the woff span of its tile is staged in shared memory.
+template <bool KEYS>
 __global__ void __launch_bounds__(kHopTile) k_hop_expand(HopArgs A) {
   __shared__ uint64_t s_woff[kHopTile + 1];
   __shared__ uint64_t s_e0, s_cnt;
@@ -177,97 +227,97 @@ __global__ void __launch_bounds__(kHopTile) k_hop_expand(HopArgs A) {
   uint32_t x, v, r;
   unpack_key(A.key_in[i], A.in_has_r, A.bits, x, v, r);
   if (x >= A.G.n || v >= A.G.n) {
-    atomicOr(A.err, 32);
-    A.key_out[item] = ~0ull;
+    if (KEYS) atomicOr(A.err, 32);
     return;
   }
   const uint64_t slot = A.sstart[i] + (item - A.woff[i]);
   if (slot >= A.roff[A.G.n]) {
-    atomicOr(A.err, 64);
-    A.key_out[item] = ~0ull;
+    if (KEYS) atomicOr(A.err, 64);
     return;
   }
   const uint32_t w = A.radj[slot];
   if (w >= A.G.n) {
-    atomicOr(A.err, 128);
-    A.key_out[item] = ~0ull;
+    if (KEYS) atomicOr(A.err, 128);
     return;
   }
-  uint64_t* row = A.row_out + item * A.P_out;
-  for (uint32_t j = 0; j < A.P_out; ++j) row[j] = 0;
-  uint64_t key = ~0ull;
-  bool any = false;
-  if (A.G.ordered || A.G.rank[w] < A.G.rank[x]) {
-    const uint32_t cx = vcol(A.G, x), cv = vcol(A.G, v), cw = vcol(A.G, w);
-    const uint32_t fin = A.first_hop ? (1u << cx) : ((1u << cx) | (1u << cv));
-    const uint32_t fout = (1u << cx) | (1u << cw);
-    const uint32_t fw = 1u << cw, fv = 1u << cv;
-    const uint64_t* prow = A.pay_in + i * A.P_in;
-    const int t_in = A.s_in - mb_popc(fin);
-    const uint64_t erow = A.etab ? (A.e_rev ? A.G.rev[slot] : slot) * A.rse : 0;
-    for (uint32_t ii = 0; ii < A.P_in; ++ii) {
-      const uint64_t pv = prow[ii];
-      if (!pv) continue;
-      const uint32_t Sin = sig_expand(sig_unrank(c_lut, t_in, ii), fin);
-      if (Sin & fw) continue;
-      const uint32_t ne = A.etab ? A.Pe : 1u;
-      for (uint32_t ie = 0; ie < ne; ++ie) {
-        uint32_t S1;
-        uint64_t v1;
-        if (A.etab) {
-          if (erow + ie >= A.n_etab) {
-            atomicOr(A.err, 256);
+  if (!(A.G.ordered || A.G.rank[w] < A.G.rank[x])) return;
+  const uint32_t cx = vcol(A.G, x), cv = vcol(A.G, v), cw = vcol(A.G, w);
+  const uint32_t fin = A.first_hop ? (1u << cx) : ((1u << cx) | (1u << cv));
+  const uint32_t fw = 1u << cw, fv = 1u << cv;
+  if (fin & fw) return;  // the new vertex repeats a key colour: no colourful extension
+  const uint32_t rr = A.record ? w : r;
+  const uint64_t key = pack_key(x, w, rr, A.out_has_r, A.bits);
+  if (KEYS) {
+    ht_insert(A.ht_key, A.ht_idx, A.ht_mask, A.ht_shift, key, A.n_keys, A.key_out);
+    return;
+  }
+  const uint32_t oi = ht_find(A.ht_key, A.ht_idx, A.ht_mask, A.ht_shift, key);
+  if (oi == ~0u) {
+    atomicOr(A.err, 64);
+    return;
+  }
+  u64* row = reinterpret_cast<u64*>(A.row_out + static_cast<uint64_t>(oi) * A.P_out);
+  const uint32_t fout = (1u << cx) | fw;
+  const uint64_t* prow = A.pay_in + i * A.P_in;
+  const int t_in = A.s_in - mb_popc(fin);
+  const uint64_t erow = A.etab ? (A.e_rev ? A.G.rev[slot] : slot) * A.rse : 0;
+  uint32_t nupd = 0;
+  for (uint32_t ii = 0; ii < A.P_in; ++ii) {
+    const uint64_t pv = prow[ii];
+    if (!pv) continue;
+    const uint32_t Sin = sig_expand(sig_unrank(c_lut, t_in, ii), fin);
+    if (Sin & fw) continue;
+    const uint32_t ne = A.etab ? A.Pe : 1u;
+    for (uint32_t ie = 0; ie < ne; ++ie) {
+      uint32_t S1;
+      uint64_t v1;
+      if (A.etab) {
+        if (erow + ie >= A.n_etab) {
+          atomicOr(A.err, 256);
+          continue;
+        }
+        const uint64_t ev = A.etab[erow + ie];
+        if (!ev) continue;
+        const uint32_t E = sig_expand(sig_unrank(c_lut, A.se - 2, ie), fv | fw);
+        if ((E & Sin) != fv) continue;
+        S1 = Sin | E;
+        v1 = mul_ck(pv, ev, A.err);
+      } else {
+        S1 = Sin | fw;
+        v1 = pv;
+      }
+      const uint32_t nn = A.ntab ? A.Pn : 1u;
+      for (uint32_t in = 0; in < nn; ++in) {
+        uint32_t S2;
+        uint64_t v2;
+        if (A.ntab) {
+          if (static_cast<uint64_t>(w) * A.rsn + in >= A.n_ntab) {
+            atomicOr(A.err, 512);
             continue;
           }
-          const uint64_t ev = A.etab[erow + ie];
-          if (!ev) continue;
-          const uint32_t E = sig_expand(sig_unrank(c_lut, A.se - 2, ie), fv | fw);
-          if ((E & Sin) != fv) continue;
-          S1 = Sin | E;
-          v1 = mul_ck(pv, ev, A.err);
+          const uint64_t nv = A.ntab[static_cast<uint64_t>(w) * A.rsn + in];
+          if (!nv) continue;
+          const uint32_t Nn = sig_expand(sig_unrank(c_lut, A.sn - 1, in), fw);
+          if ((Nn & S1) != fw) continue;
+          S2 = S1 | Nn;
+          v2 = mul_ck(v1, nv, A.err);
         } else {
-          S1 = Sin | fw;
-          v1 = pv;
+          S2 = S1;
+          v2 = v1;
         }
-        const uint32_t nn = A.ntab ? A.Pn : 1u;
-        for (uint32_t in = 0; in < nn; ++in) {
-          uint32_t S2;
-          uint64_t v2;
-          if (A.ntab) {
-            if (static_cast<uint64_t>(w) * A.rsn + in >= A.n_ntab) {
-              atomicOr(A.err, 512);
-              continue;
-            }
-            const uint64_t nv = A.ntab[static_cast<uint64_t>(w) * A.rsn + in];
-            if (!nv) continue;
-            const uint32_t Nn = sig_expand(sig_unrank(c_lut, A.sn - 1, in), fw);
-            if ((Nn & S1) != fw) continue;
-            S2 = S1 | Nn;
-            v2 = mul_ck(v1, nv, A.err);
-          } else {
-            S2 = S1;
-            v2 = v1;
-          }
-          const uint32_t o = sig_index(c_lut, S2, fout);
-          if (o >= A.P_out || mb_popc(S2) != A.s_out) {
-            atomicOr(A.err, 16);  // signature outside the frontier row: plan/popcount bug
-            continue;
-          }
-          row[o] = add_ck(row[o], v2, A.err);
-          any = true;
+        const uint32_t o = sig_index(c_lut, S2, fout);
+        if (o >= A.P_out || mb_popc(S2) != A.s_out) {
+          atomicOr(A.err, 16);  // signature outside the frontier row: plan/popcount bug
+          continue;
         }
+        atomic_add_ck(row + o, v2, A.err);
+        ++nupd;
       }
     }
-    if (any) {
-      const uint32_t rr = A.record ? w : r;
-      key = pack_key(x, w, rr, A.out_has_r, A.bits);
-    }
   }
-  A.key_out[item] = key;
   const unsigned am = __activemask();
-  const unsigned bal = __ballot_sync(am, any);
-  if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(am) - 1) && bal)
-    atomicAdd(A.updates, static_cast<u64>(__popc(bal)));
+  const unsigned tot = __reduce_add_sync(am, nupd);
+  if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(am) - 1) && tot) atomicAdd(A.updates, static_cast<u64>(tot));
 }
 
 template <class T>
@@ -322,6 +372,10 @@ struct MergeArgs {
   const uint64_t* keyB;
   const uint64_t* payB;
   uint64_t nB;
+  const uint64_t* htB_key;  // B's hash table (key -> entry)
+  const uint32_t* htB_idx;
+  uint64_t htB_mask;
+  int htB_shift;
   int sB;
   uint32_t PB;
   int bits;
@@ -354,16 +408,13 @@ __global__ void __launch_bounds__(256) k_half_merge(MergeArgs A) {
     uint32_t x, v, r;
     unpack_key(A.keyA[i], A.A_has_r, A.bits, x, v, r);
     const uint64_t kb = (static_cast<uint64_t>(x) << A.bits) | v;
-    uint64_t lo = 0, hi = A.nB;
-    while (lo < hi) {
-      const uint64_t mid = (lo + hi) >> 1;
-      if (A.keyB[mid] < kb) lo = mid + 1; else hi = mid;
-    }
+    const uint32_t bi = A.nB ? ht_find(A.htB_key, A.htB_idx, A.htB_mask, A.htB_shift, kb) : ~0u;
+    const uint64_t lo = bi;
     if (A.out_kind == 4) {
       A.ckey[i] = ~0ull;
       for (uint32_t j = 0; j < A.Pout; ++j) A.crow[i * A.Pout + j] = 0;
     }
-    bool found = lo < A.nB && A.keyB[lo] == kb;
+    bool found = bi != ~0u;
     uint64_t orow = 0;
     uint32_t ofix = 0;
     const uint32_t ids[3] = {x, v, r};
@@ -436,11 +487,14 @@ struct CycleDesc {
 };
 
 struct Frontier {
-  DBuf key, pay;
+  DBuf key, pay;  // entries in insertion order (not sorted)
   uint64_t n = 0;
   int s = 0;
   uint32_t P = 0;
   int has_r = 0;
+  DBuf ht_key, ht_idx;  // hash table key -> entry (built by the hop that produced it)
+  uint64_t ht_mask = 0;
+  int ht_shift = 64;
 };
 
 // Rows of a relation as seen when walking from the first key to the second.
@@ -512,6 +566,13 @@ struct CycleRunner {
   static uint64_t binom(int a, int b) { return binom_host(a, b); }
 
   double wait_s = 0;  // host time blocked in d2h (MB_DEBUG_BATCH)
+
+  bool overflowed() {
+    int e = 0;
+    MB_CUDA(cudaMemcpyAsync(&e, err, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    MB_CUDA(cudaStreamSynchronize(stream));
+    return (e & 1) != 0;
+  }
 
   uint64_t d2h(const uint64_t* p) {
     uint64_t v = 0;
@@ -586,11 +647,23 @@ struct CycleRunner {
     scan(work.as<uint64_t>(), woff.as<uint64_t>(), in.n + 1);
     const uint64_t W = d2h(woff.as<uint64_t>() + in.n);
     if (W == 0) return true;
-    if (W * (out.P * 8ull + 72) > mem_budget && !force_hop) {
-      last_over = W * (out.P * 8ull + 72);
+    // scratch: 2W hash slots (12 B), W keys, and at most W rows
+    if (W * (out.P * 8ull + 40) > mem_budget && !force_hop) {
+      last_over = W * (out.P * 8ull + 40);
       return false;
     }
-    DBuf keys(W * 8), rows(W * out.P * 8);
+    // hash table: a power of two >= 2 W slots (load <= 1/2)
+    int lg = 1;
+    while ((1ull << lg) < 2 * W) ++lg;
+    const uint64_t cap = 1ull << lg;
+    out.ht_key.alloc(cap * 8);
+    out.ht_idx.alloc(cap * 4);
+    out.ht_mask = cap - 1;
+    out.ht_shift = 64 - lg;
+    MB_CUDA(cudaMemsetAsync(out.ht_key.p, 0xFF, cap * 8, stream));
+    out.key.alloc(W * 8);
+    DBuf nk(8);
+    MB_CUDA(cudaMemsetAsync(nk.p, 0, 8, stream));
     HopArgs A{};
     A.G = G;
     A.key_in = in.key.as<uint64_t>();
@@ -612,22 +685,34 @@ struct CycleRunner {
     A.P_out = out.P;
     A.out_has_r = out.has_r;
     A.bits = bits;
-    A.key_out = keys.as<uint64_t>();
-    A.row_out = rows.as<uint64_t>();
+    A.key_out = out.key.as<uint64_t>();
+    A.ht_key = out.ht_key.as<uint64_t>();
+    A.ht_idx = out.ht_idx.as<uint32_t>();
+    A.ht_mask = out.ht_mask;
+    A.ht_shift = out.ht_shift;
+    A.n_keys = reinterpret_cast<unsigned long long*>(nk.p);
     A.err = err;
     A.updates = upd;
     static const bool dbg = std::getenv("MB_DEBUG_HOPS") != nullptr;
+    // compulsory bytes: per item its neighbour id, colour and one probe
+    // (8-byte key) per pass; per input entry its key, work offsets and row;
+    // per output key its slot and row
+    const uint64_t hop_bytes = W * (4 + 1 + 2 * 8) + in.n * (8 + 16 + 8ull * in.P);
+    launch("cycle_hop_keys", [&] { k_hop_expand<true><<<grid_for(W, kHopTile), kHopTile, 0, stream>>>(A); },
+           hop_bytes / 2);
+    out.n = d2h(nk.as<uint64_t>());
+    out.pay.alloc(std::max<uint64_t>(out.n * out.P, 1) * 8);
+    if (out.n) MB_CUDA(cudaMemsetAsync(out.pay.p, 0, out.n * out.P * 8, stream));
+    A.row_out = out.pay.as<uint64_t>();
+    if (out.n)
+      launch("cycle_hop_expand", [&] { k_hop_expand<false><<<grid_for(W, kHopTile), kHopTile, 0, stream>>>(A); },
+             hop_bytes / 2 + out.n * (8 + 8ull * out.P));
     if (dbg)
-      fprintf(stderr, "hop n_in=%llu W=%llu s_in=%d P_in=%u first=%d in_r=%d out_r=%d rec=%d s_out=%d P_out=%u "
-              "etab=%p Pe=%u se=%d rse=%u erev=%d n_etab=%llu ntab=%p Pn=%u sn=%d rsn=%u bits=%d\n",
-              (unsigned long long)in.n, (unsigned long long)W, in.s, in.P, (int)first, in.has_r, out.has_r,
-              (int)record, out.s, out.P, (const void*)A.etab, A.Pe, A.se, A.rse, A.e_rev,
-              (unsigned long long)A.n_etab, (const void*)A.ntab, A.Pn, A.sn, A.rsn, bits);
-    // compulsory bytes: per item its neighbour id, colour, output key and
-    // row; per input entry its key, work offsets and row
-    const uint64_t hop_bytes = W * (4 + 1 + 8 + 8ull * out.P) + in.n * (8 + 16 + 8ull * in.P);
-    launch("cycle_hop_expand", [&] { k_hop_expand<<<grid_for(W, kHopTile), kHopTile, 0, stream>>>(A); }, hop_bytes);
-    aggregate(keys, rows, W, out.P, out.key, out.pay, out.n, (out.has_r ? 3 : 2) * bits);
+      fprintf(stderr, "hop n_in=%llu W=%llu keys=%llu s_in=%d P_in=%u first=%d in_r=%d out_r=%d rec=%d s_out=%d "
+              "P_out=%u etab=%p Pe=%u ntab=%p Pn=%u bits=%d\n",
+              (unsigned long long)in.n, (unsigned long long)W, (unsigned long long)out.n, in.s, in.P, (int)first,
+              in.has_r, out.has_r, (int)record, out.s, out.P, (const void*)A.etab, A.Pe, (const void*)A.ntab, A.Pn,
+              bits);
     return true;
   }
 
@@ -732,6 +817,9 @@ struct CycleRunner {
     M.keyA = A.key.as<uint64_t>(), M.payA = A.pay.as<uint64_t>(), M.nA = A.n, M.sA = A.s, M.PA = A.P;
     M.A_has_r = A.has_r;
     M.keyB = B.key.as<uint64_t>(), M.payB = B.pay.as<uint64_t>(), M.nB = B.n, M.sB = B.s, M.PB = B.P;
+    if (B.n && !B.ht_key.p) fail(kInternal, "half-path frontier without a hash table");
+    M.htB_key = B.ht_key.as<uint64_t>(), M.htB_idx = B.ht_idx.as<uint32_t>();
+    M.htB_mask = B.ht_mask, M.htB_shift = B.ht_shift;
     M.bits = bits;
     M.out_kind = C.out.kind == 1 ? 1 : (C.out.kind == 2 ? 2 : (C.out.kind == 3 ? 3 : 4));
     M.key_src0 = ks0, M.key_src1 = ks1;
@@ -888,6 +976,16 @@ struct CycleRunner {
         if (run_batch(C, h, x0, nx)) {
           ++ok;
           x0 += nx;
+          // fail fast: every contribution is non-negative and the anchors run
+          // hubs first, so once a checked add or multiply has overflowed the
+          // count is >= 2^64 and the reference's checked arithmetic raises
+          // OverflowError as well (errors.hpp:38-50, ProjectionTable::add at
+          // table.cpp:38-54): stop here,
+          // count() turns the flag into that error
+          if (overflowed()) {
+            if (dbg) fprintf(stderr, "cycle L=%d: overflow after anchor %u of %u\n", C.L, x0, G.n);
+            return;
+          }
           // anchors get lighter along the sweep: grow, but only slowly past a failure
           cap = static_cast<uint32_t>(std::min<uint64_t>(first_batch, cap + cap / 4 + 1));
           bs = static_cast<uint32_t>(std::min<uint64_t>(2ull * nx, cap));

@@ -256,8 +256,11 @@ __global__ void k_recolor(uint32_t n, int C, const uint8_t* __restrict__ in, uin
   for (int c = 0; c < kChiStride; ++c) {
     if (c < C) {
       const int cc = in[static_cast<uint64_t>(c) * n + src];
-      if (cc < 1 || cc > k) atomicOr(err, 2);
-      cols |= static_cast<unsigned long long>((cc - 1) & 0xFF) << (8 * c);
+      // an invalid colour raises SpecError after the batch; it is replaced by
+      // colour 0 so that no kernel indexes its colour tables with it
+      const bool ok = cc >= 1 && cc <= k;
+      if (!ok) atomicOr(err, 2);
+      cols |= static_cast<unsigned long long>(ok ? cc - 1 : 0) << (8 * c);
     }
   }
   reinterpret_cast<unsigned long long*>(out)[v] = cols;

@@ -33,9 +33,12 @@ struct EngineStats {
   double prep_ms = 0;           // wall time of the last plan-derived index build
 };
 
+int current_device();  // the calling thread's current CUDA device
+
 class GpuEngine {
  public:
-  explicit GpuEngine(const CsrGraph& g, int device = 0);
+  // device < 0: the caller's current CUDA device
+  explicit GpuEngine(const CsrGraph& g, int device = -1);
   ~GpuEngine();
   GpuEngine(const GpuEngine&) = delete;
   GpuEngine& operator=(const GpuEngine&) = delete;
@@ -67,6 +70,7 @@ class GpuEngine {
   uint64_t launches() const;
   const EngineStats& stats() const;
   void* stream() const;
+  int device() const;
 
   struct Impl;
 

@@ -1,16 +1,23 @@
-"""Multi-GPU counting: one process per GPU, colourings sharded across ranks.
+"""Multi-GPU counting: one process per GPU.
 
-The reference parallelises one colouring's DP over p workers with a 1-D
-vertex partition and entry exchange between rounds (runtime.hpp:14-88,
-BspExecutor), and estimate() runs trials in parallel threads
-(estimate.cpp:149).  On B200 a whole colouring of the benchmark graphs fits
-one GPU (the largest config's tables are a few GB of 180 GB HBM), so the
-independent units are the colourings: rank r counts the contiguous block of
-colourings that Partition(num_colourings, world).block(r) assigns it, with no
-data-path collective, and the per-colouring counts are all-gathered once at
-the end (NCCL on GPUs, gloo on CPU).  Results are bit-identical to the
-single-GPU call for every world size.
+Two shardings, both without a data-path collective:
 
+* colourings (``distributed_count_seeds`` / ``distributed_estimate``): rank r
+  counts the contiguous block of colourings that Partition(num_colourings,
+  world).block(r) assigns it (runtime.hpp:14-36), each on its own GPU with the
+  whole graph resident, and the per-colouring counts are all-gathered once at
+  the end (NCCL on GPUs, gloo on CPU).  This is the layout for plans whose
+  tables fit one GPU (configs 0 and 1) and for estimate()'s independent trials
+  (estimate.cpp:149).
+* vertices (``distributed_count_vertex_sharded``): one colouring's root block
+  is split by anchor vertex, the data-graph vertices being dealt to ranks as
+  the reference's Partition deals them to BSP workers (runtime.cpp:11-25, here
+  cyclically over the degree order so every rank gets its share of hubs); each
+  rank sums the matches anchored at its own vertices and the partial counts
+  are added with one all-reduce (the reference's sharded total,
+  runtime.cpp:297-302).  See DESIGN.md §6.
+
+Results are bit-identical to the single-GPU call for every world size.
 ``count_fn`` lets the CPU tests drive the same plumbing with the oracle.
 """
 from __future__ import annotations
@@ -19,7 +26,7 @@ from typing import Callable, Sequence
 
 import numpy as np
 
-from . import EstimateReport, automorphism_count, coefficient_of_variation, derive_seed, normalization_factor
+from . import EstimateReport, derive_seed, estimate_from_counts
 
 
 def block(n: int, world: int, rank: int) -> tuple[int, int]:
@@ -88,9 +95,4 @@ def distributed_estimate(g, plan, engine: int, trials: int, seed: int, k: int | 
     edges = plan.edges if edges is None else edges
     seeds = [derive_seed(seed, i) for i in range(trials)]
     per = distributed_count_seeds(g, plan, seeds, engine, count_fn, device)
-    norm = normalization_factor(k)
-    total = sum(int(x) for x in per)
-    mean = norm * (total / trials)
-    aut = automorphism_count(k, edges)
-    return EstimateReport(trials, [int(x) for x in per], norm, mean, coefficient_of_variation(per), aut,
-                          mean / aut)
+    return estimate_from_counts(k, edges, per)

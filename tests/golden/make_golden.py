@@ -40,8 +40,12 @@ QUERIES = {
     "c7": (7, [(i, (i + 1) % 7) for i in range(7)]),
     "q6": (6, [(0, 1), (1, 2), (2, 0), (1, 3), (3, 2), (2, 4), (4, 5)]),
     "theta": (8, [(0, 1), (1, 2), (2, 7), (0, 3), (3, 4), (4, 7), (0, 5), (5, 6), (6, 7)]),
+    # BASELINE config 4: 6-cycle with chords 0-2 and 3-5, path 1-6-7-8 and triangle 8-9-1 (14 edges)
     "sp10": (10, [(0, 1), (1, 2), (2, 3), (3, 4), (4, 5), (5, 0), (0, 2), (3, 5), (1, 6), (6, 7), (7, 8),
-                  (8, 9), (9, 1)]),
+                  (8, 9), (9, 1), (1, 8)]),
+    # the same without the chord 1-8 (a 5-cycle 1-6-7-8-9 instead of the triangle)
+    "sp10_open": (10, [(0, 1), (1, 2), (2, 3), (3, 4), (4, 5), (5, 0), (0, 2), (3, 5), (1, 6), (6, 7), (7, 8),
+                       (8, 9), (9, 1)]),
     "sat": (11, [(0, 1), (1, 2), (2, 3), (3, 4), (4, 0), (0, 5), (2, 6), (5, 6), (5, 7), (5, 8), (6, 8),
                  (8, 9), (9, 10), (10, 8)]),
     "brain1": (9, [(0, 1), (1, 2), (2, 3), (3, 0), (0, 4), (4, 5), (5, 6), (6, 7), (7, 8), (8, 0)]),

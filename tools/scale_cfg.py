@@ -25,4 +25,4 @@ for sz in sys.argv[2:]:
               mb.engine_stats(g), flush=True)
     except Exception as e:
         print(f"size {sz} n={g.num_vertices()} m={g.num_edges()} FAILED after {time.time()-t:.1f}s: {e}", flush=True)
-        break
+        continue
