@@ -95,6 +95,15 @@ int mb_count_colorful(mb_graph* g, mb_plan* p, const uint8_t* chi, int ncol, int
 /* Same, colourings generated from seeds with random_coloring(n, k, seed). */
 int mb_count_colorful_seeds(mb_graph* g, mb_plan* p, const uint64_t* seeds, int ncol, int engine,
                             uint64_t* out);
+/* Vertex-sharded count (one rank of a multi-GPU job; the
+ * reference's BspExecutor over Partition, runtime.cpp:11-25, 297-324): this
+ * rank's partial count of each colouring, the matches of the root block
+ * anchored at its share of the data-graph vertices (device vertices in degree
+ * order dealt cyclically over `world` ranks).  The partials of ranks
+ * 0..world-1 add up to mb_count_colorful's count.  *split (nullable) = 1 when
+ * the root block was split, 0 when rank 0 returned the whole count. */
+int mb_count_colorful_shard(mb_graph* g, mb_plan* p, const uint8_t* chi, int ncol, int engine,
+                            int rank, int world, uint64_t* partial, int* split);
 /* Device-resident colourings (n*ncol bytes, colours 1..k, cudaMalloc'd). */
 int mb_count_colorful_device(mb_graph* g, mb_plan* p, const uint8_t* chi_dev, int ncol,
                              uint64_t* out);

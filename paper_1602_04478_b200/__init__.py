@@ -42,7 +42,7 @@ __all__ = [
     "MotifError", "ParseError", "TreewidthError", "CountOverflowError", "BudgetError",
     "SchemaError", "ContractError", "SpecError", "CudaError",
     "DataGraph", "QueryPlan", "EstimateReport", "Partition", "load_edge_list", "degree_rank",
-    "random_coloring", "derive_seed", "count_colorful", "estimate", "automorphism_count",
+    "random_coloring", "derive_seed", "count_colorful", "count_colorful_shard", "estimate", "automorphism_count",
     "normalization_factor", "coefficient_of_variation", "estimate_from_counts", "PS", "DB", "lib",
 ]
 
@@ -129,6 +129,8 @@ def _load() -> C.CDLL:
         "mb_count_colorful": (C.c_int, [P, P, u8p, C.c_int, C.c_int, u64p]),
         "mb_count_colorful_seeds": (C.c_int, [P, P, u64p, C.c_int, C.c_int, u64p]),
         "mb_count_colorful_device": (C.c_int, [P, P, C.c_void_p, C.c_int, u64p]),
+        "mb_count_colorful_shard": (C.c_int, [P, P, u8p, C.c_int, C.c_int, C.c_int, C.c_int, u64p,
+                                              C.POINTER(C.c_int)]),
         "mb_automorphism_count": (C.c_int, [C.c_int, i32p, C.c_int, u64p]),
         "mb_normalization_factor": (C.c_double, [C.c_int]),
         "mb_coefficient_of_variation": (C.c_double, [u64p, C.c_uint64]),
@@ -347,6 +349,21 @@ def count_colorful_seeds(g: DataGraph, plan: QueryPlan, seeds: Iterable[int], en
     _check(lib.mb_count_colorful_seeds(g.handle, plan.handle, _ptr(s, C.c_uint64), len(s), engine,
                                        _ptr(out, C.c_uint64)))
     return out
+
+
+def count_colorful_shard(g: DataGraph, plan: QueryPlan, chi: np.ndarray, rank: int, world: int,
+                         engine: int = DB) -> tuple[np.ndarray, bool]:
+    """This rank's partial counts of a vertex-sharded count (one per colouring)
+    and whether the root block was split; partials of all ranks add up to
+    count_colorful's counts (mb_count_colorful_shard)."""
+    a = np.ascontiguousarray(np.atleast_2d(chi), dtype=np.uint8)
+    if a.shape[1] != g.num_vertices():
+        raise SpecError("colouring length != number of vertices")
+    out = np.zeros(a.shape[0], dtype=np.uint64)
+    split = C.c_int()
+    _check(lib.mb_count_colorful_shard(g.handle, plan.handle, _ptr(a, C.c_uint8), a.shape[0], engine, rank, world,
+                                       _ptr(out, C.c_uint64), C.byref(split)))
+    return out, bool(split.value)
 
 
 def count_colorful_device(g: DataGraph, plan: QueryPlan, chi_dev_ptr: int, ncol: int) -> np.ndarray:

@@ -257,6 +257,24 @@ int mb_count_colorful_seeds(mb_graph* g, mb_plan* p, const uint64_t* seeds, int 
   });
 }
 
+int mb_count_colorful_shard(mb_graph* g, mb_plan* p, const uint8_t* chi, int ncol, int engine, int rank, int world,
+                            uint64_t* partial, int* split) {
+  return guarded([&] {
+    if (engine != 0 && engine != 1) mb::fail(mb::kSpec, "engine must be 0 (PS) or 1 (DB)");
+    if (world < 1 || rank < 0 || rank >= world) mb::fail(mb::kSpec, "shard rank out of range");
+    auto& eng = engine_for(g, p);
+    if (split) *split = eng.root_shardable() ? 1 : 0;
+    eng.set_shard(static_cast<uint32_t>(rank), static_cast<uint32_t>(world));
+    try {
+      eng.count(chi, ncol, true, partial);
+    } catch (...) {
+      eng.set_shard(0, 1);
+      throw;
+    }
+    eng.set_shard(0, 1);
+  });
+}
+
 int mb_count_colorful_device(mb_graph* g, mb_plan* p, const uint8_t* chi_dev, int ncol, uint64_t* out) {
   return guarded([&] { engine_for(g, p).count(chi_dev, ncol, false, out); });
 }

@@ -122,6 +122,36 @@ __device__ __forceinline__ void ht_insert(uint64_t* ht_key, uint32_t* ht_idx, ui
   }
 }
 
+// Dense index of `key` in a table that is read and written by the same
+// launch (the pair table of k_half_merge): inserts on first use; a thread
+// that finds the key before its inserter has published the index waits for
+// it (ht_idx starts as all ~0u).
+__device__ __forceinline__ uint32_t ht_get(uint64_t* ht_key, uint32_t* ht_idx, uint64_t mask, int shift, uint64_t key,
+                                           unsigned long long* n_keys, uint64_t* key_out) {
+  uint64_t h = ht_slot(key, shift);
+  while (true) {
+    uint64_t cur = *reinterpret_cast<volatile uint64_t*>(ht_key + h);
+    if (cur == kEmptyKey) {
+      cur = atomicCAS(reinterpret_cast<unsigned long long*>(ht_key + h), kEmptyKey, key);
+      if (cur == kEmptyKey) {
+        const uint32_t idx = static_cast<uint32_t>(atomicAdd(n_keys, 1ull));
+        key_out[idx] = key;
+        __threadfence();
+        atomicExch(ht_idx + h, idx);
+        return idx;
+      }
+    }
+    if (cur == key) {
+      uint32_t idx;
+      do {
+        idx = *reinterpret_cast<volatile uint32_t*>(ht_idx + h);
+      } while (idx == ~0u);
+      return idx;
+    }
+    h = (h + 1) & mask;
+  }
+}
+
 // Dense index of a key known to be present (after the keys pass), or ~0u.
 __device__ __forceinline__ uint32_t ht_find(const uint64_t* __restrict__ ht_key, const uint32_t* __restrict__ ht_idx,
                                             uint64_t mask, int shift, uint64_t key) {
@@ -174,6 +204,26 @@ __global__ void k_hop_work(const uint64_t* __restrict__ key_in, uint64_t n_in, i
   }
   sstart[i] = lo;
   work[i] = hi - lo;
+}
+
+// S2[x] = sum of deg(v) over the suffix neighbours v of x (ids above x in the
+// degree order): an upper bound of the second hop's work from anchor x.
+__global__ void k_suffix_work(uint32_t n, const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
+                              uint64_t* __restrict__ s2) {
+  const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= n) return;
+  uint64_t lo = off[x], hi = off[x + 1];
+  uint64_t a = lo, b = hi;
+  while (a < b) {
+    const uint64_t mid = (a + b) >> 1;
+    if (adj[mid] <= x) a = mid + 1; else b = mid;
+  }
+  uint64_t t = 0;
+  for (uint64_t e = a; e < hi; ++e) {
+    const uint32_t v = adj[e];
+    t += off[v + 1] - off[v];
+  }
+  s2[x] = t;
 }
 
 constexpr int kHopTile = 256;  // items per CTA of k_hop_expand
@@ -346,12 +396,14 @@ __global__ void k_seg_accumulate(const uint64_t* __restrict__ keys, const uint32
     if (row[j]) atomic_add_ck(reinterpret_cast<u64*>(pay_out + seg * P + j), row[j], err);
 }
 
-__global__ void k_init_frontier(uint32_t x0, uint32_t nx, int bits, const uint8_t* __restrict__ chi,
+// Frontier of the anchors x0, x0 + stride, ... (nx of them): stride > 1 when
+// the anchors are dealt cyclically over ranks (vertex-sharded root block).
+__global__ void k_init_frontier(uint32_t x0, uint32_t nx, uint32_t stride, int bits, const uint8_t* __restrict__ chi,
                                 const uint64_t* __restrict__ utab, uint32_t Pu, uint32_t rsu,
                                 uint64_t* __restrict__ key, uint64_t* __restrict__ pay) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= nx) return;
-  const uint64_t x = x0 + i;
+  const uint64_t x = x0 + static_cast<uint64_t>(i) * stride;
   key[i] = (x << bits) | x;
   if (utab) {
     for (uint32_t j = 0; j < Pu; ++j) pay[static_cast<uint64_t>(i) * Pu + j] = utab[x * rsu + j];
@@ -381,8 +433,14 @@ struct MergeArgs {
   int bits;
   // output
   int out_kind;  // 1 scalar, 2 vertex, 3 edge, 4 pair (contribution rows)
-  uint64_t* ckey;   // pair: [nA] keys (UINT64_MAX = none)
-  uint64_t* crow;   // pair: [nA][Pout]
+  // pair outputs: the running pair hash table (key -> dense row index)
+  uint64_t* ph_key;
+  uint32_t* ph_idx;
+  uint64_t ph_mask;
+  int ph_shift;
+  unsigned long long* ph_n;
+  uint64_t* ph_list;  // dense index -> key
+  uint64_t* ph_rows;  // [dense index][Pout]
   int key_src0, key_src1;  // 0 = x, 1 = v, 2 = r
   uint64_t* out;
   uint32_t Pout, rso;
@@ -410,10 +468,6 @@ __global__ void __launch_bounds__(256) k_half_merge(MergeArgs A) {
     const uint64_t kb = (static_cast<uint64_t>(x) << A.bits) | v;
     const uint32_t bi = A.nB ? ht_find(A.htB_key, A.htB_idx, A.htB_mask, A.htB_shift, kb) : ~0u;
     const uint64_t lo = bi;
-    if (A.out_kind == 4) {
-      A.ckey[i] = ~0ull;
-      for (uint32_t j = 0; j < A.Pout; ++j) A.crow[i * A.Pout + j] = 0;
-    }
     bool found = bi != ~0u;
     uint64_t orow = 0;
     uint32_t ofix = 0;
@@ -436,9 +490,13 @@ __global__ void __launch_bounds__(256) k_half_merge(MergeArgs A) {
         orow = static_cast<uint64_t>(y) * A.rso;
         ofix = 1u << vcol(A.G, y);
       } else if (A.out_kind == 4) {
+        // the reference's arity-2 merge output (table.cpp:225-275): rows of
+        // the running pair hash table, inserted on first use; the host keeps
+        // its capacity above the number of A entries of every launch
         const uint32_t p = ids[A.key_src0], q = ids[A.key_src1];
-        A.ckey[i] = (static_cast<uint64_t>(p) << A.bits) | q;
-        orow = i * A.Pout;
+        const uint64_t key = (static_cast<uint64_t>(p) << A.bits) | q;
+        const uint32_t di = ht_get(A.ph_key, A.ph_idx, A.ph_mask, A.ph_shift, key, A.ph_n, A.ph_list);
+        orow = static_cast<uint64_t>(di) * A.Pout;
         ofix = (1u << vcol(A.G, p)) | (1u << vcol(A.G, q));
       }
       const uint64_t* ra = A.payA + i * A.PA;
@@ -458,8 +516,7 @@ __global__ void __launch_bounds__(256) k_half_merge(MergeArgs A) {
           if (A.out_kind == 1) {
             local = add_ck(local, val, A.err);
           } else if (A.out_kind == 4) {
-            uint64_t* c = A.crow + orow + sig_index(c_lut, Sa | Sb, ofix);
-            *c = add_ck(*c, val, A.err);
+            atomic_add_ck(reinterpret_cast<u64*>(A.ph_rows + orow + sig_index(c_lut, Sa | Sb, ofix)), val, A.err);
           } else {
             atomic_add_ck(reinterpret_cast<u64*>(A.out + orow + sig_index(c_lut, Sa | Sb, ofix)), val, A.err);
           }
@@ -530,6 +587,25 @@ __global__ void k_swap_pair_keys(const uint64_t* __restrict__ in, uint64_t nk, i
   out[i] = ((in[i] & mask) << bits) | (in[i] >> bits);
 }
 
+__global__ void k_gather_rows32(const uint32_t* __restrict__ idx, const uint64_t* __restrict__ in, uint32_t P,
+                                uint64_t nk, uint64_t* __restrict__ out) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= nk * P) return;
+  const uint64_t r = i / P, j = i - r * P;
+  out[i] = in[static_cast<uint64_t>(idx[r]) * P + j];
+}
+
+// Re-inserts the dense keys 0..n-1 of a pair table into a larger hash table.
+__global__ void k_pair_rehash(const uint64_t* __restrict__ list, uint64_t n, uint64_t* __restrict__ ht_key,
+                              uint32_t* __restrict__ ht_idx, uint64_t mask, int shift) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= n) return;
+  const uint64_t key = list[i];
+  uint64_t h = ht_slot(key, shift);
+  while (atomicCAS(reinterpret_cast<unsigned long long*>(ht_key + h), kEmptyKey, key) != kEmptyKey) h = (h + 1) & mask;
+  ht_idx[h] = static_cast<uint32_t>(i);
+}
+
 __global__ void k_gather_rows(const uint64_t* __restrict__ idx, const uint64_t* __restrict__ in, uint32_t P,
                               uint64_t nk, uint64_t* __restrict__ out) {
   const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
@@ -538,12 +614,12 @@ __global__ void k_gather_rows(const uint64_t* __restrict__ idx, const uint64_t* 
   out[i] = in[idx[r] * P + j];
 }
 
-struct PairBuild {  // merge contributions of a pair-keyed block
-  std::vector<DBuf> keys, rows;
-  std::vector<uint64_t> counts;
-  uint64_t pending = 0;  // contributions not yet folded into the running table
-  DBuf run_key, run_pay;  // running aggregate (sorted distinct keys)
-  uint64_t run_n = 0;
+struct PairHash {  // running pair-keyed output of a block (merge contributions)
+  DBuf key, idx;     // open-addressing slots (2 x rows)
+  DBuf list, rows;   // dense index -> key, [dense index][P] u64
+  DBuf counter;      // number of keys (device)
+  uint64_t cap_rows = 0, n = 0;  // row capacity, keys after the last merge (host)
+  int shift = 64;
 };
 
 struct CycleRunner {
@@ -561,7 +637,12 @@ struct CycleRunner {
   uint64_t mem_budget = 6ull << 30;  // bytes of per-hop scratch per batch
   bool force = false;                 // single-anchor batch: no further split
   uint32_t h_mult = 1;                // Eq. 1 terms represented by each evaluated h
-  PairBuild pairs;
+  PairHash pairs;
+  // pair-table streaming (engine_host.inc, streamed_root_of): called with a
+  // full running table; it builds the partial table, evaluates the root on it
+  // and drops it
+  std::function<void()> pair_flush;
+  uint64_t pair_flush_bytes = ~0ull;
 
   static uint64_t binom(int a, int b) { return binom_host(a, b); }
 
@@ -629,6 +710,8 @@ struct CycleRunner {
 
   // Returns false when the hop exceeded the scratch budget (caller splits the batch).
   uint64_t last_over = 0;  // scratch bytes the last refused hop needed
+  uint64_t batch_need = 0;  // largest hop scratch of the current batch
+  std::function<const std::vector<double>&()> s2_prefix;  // prefix sums of S2 (host, per graph)
 
   bool hop(const Frontier& in, Frontier& out, const Relation& rel, const TabView& nt, bool record, bool first,
            bool force_hop) {
@@ -648,6 +731,7 @@ struct CycleRunner {
     const uint64_t W = d2h(woff.as<uint64_t>() + in.n);
     if (W == 0) return true;
     // scratch: 2W hash slots (12 B), W keys, and at most W rows
+    batch_need = std::max<uint64_t>(batch_need, W * (out.P * 8ull + 40));
     if (W * (out.P * 8ull + 40) > mem_budget && !force_hop) {
       last_over = W * (out.P * 8ull + 40);
       return false;
@@ -790,9 +874,23 @@ struct CycleRunner {
     return true;
   }
 
-  // Builds the half path from h towards d for anchors [x0, x0 + nx).
+  // Vertex sharding of a root block: this rank anchors the
+  // device vertices x with x % shard_world == shard_rank.  Device ids follow
+  // the degree order, so the cyclic deal gives every rank its share of hubs.
+  uint32_t shard_rank = 0, shard_world = 1;
+
+  // Builds the half path from h towards d for the owned anchors in [x0, x0 + nx).
   bool half(const CycleDesc& C, int h, int d, bool cw, bool start_ann, bool end_ann, int rec_pos, uint32_t x0,
             uint32_t nx, const Sink& sink) {
+    {
+      // first owned anchor at or after x0, and how many owned ones the range holds
+      const uint32_t W = shard_world;
+      const uint32_t first = x0 + ((shard_rank + W - x0 % W) % W);
+      const uint64_t end = static_cast<uint64_t>(x0) + nx;
+      nx = first < end ? static_cast<uint32_t>((end - 1 - first) / W + 1) : 0;
+      x0 = first;
+      if (nx == 0) return true;
+    }
     Frontier cur;
     const TabView& hn = C.node[h];
     const bool use_start = start_ann && hn.kind;
@@ -803,7 +901,8 @@ struct CycleRunner {
     cur.key.alloc(std::max<uint32_t>(nx, 1) * 8);
     cur.pay.alloc(std::max<uint64_t>(static_cast<uint64_t>(nx) * cur.P, 1) * 8);
     launch("cycle_init", [&] {
-      k_init_frontier<<<grid_for(nx, 256), 256, 0, stream>>>(x0, nx, bits, G.chi, use_start ? hn.data : nullptr,
+      k_init_frontier<<<grid_for(nx, 256), 256, 0, stream>>>(x0, nx, shard_world, bits, G.chi,
+                                                             use_start ? hn.data : nullptr,
                                                              cur.P, hn.rs, cur.key.as<uint64_t>(),
                                                              cur.pay.as<uint64_t>());
     });
@@ -826,55 +925,61 @@ struct CycleRunner {
     M.out = C.out.data, M.Pout = C.out.P, M.rso = C.out.rs;
     M.scalar = scalar, M.err = err, M.updates = upd;
     M.scalar_mult = h_mult;
-    DBuf ck, cr;
     if (M.out_kind == 4) {
-      ck.alloc(A.n * 8);
-      cr.alloc(std::max<uint64_t>(A.n * C.out.P, 1) * 8);
-      M.ckey = ck.as<uint64_t>(), M.crow = cr.as<uint64_t>();
+      ArenaScope no_arena(nullptr);  // the pair table outlives the anchor batch
+      // streaming into the root: a full partial table is consumed first
+      if (pair_flush && pairs.n && pairs.n * (C.out.P + 2) * 8ull > pair_flush_bytes) pair_flush();
+      reserve_pairs(C.out.P, pairs.n + A.n);
+      M.ph_key = pairs.key.as<uint64_t>(), M.ph_idx = pairs.idx.as<uint32_t>();
+      M.ph_mask = 2 * pairs.cap_rows - 1, M.ph_shift = pairs.shift;
+      M.ph_n = reinterpret_cast<unsigned long long*>(pairs.counter.p);
+      M.ph_list = pairs.list.as<uint64_t>(), M.ph_rows = pairs.rows.as<uint64_t>();
     }
     launch("cycle_merge", [&] { k_half_merge<<<grid_for(A.n, 256), 256, 0, stream>>>(M); });
-    if (M.out_kind == 4) {
-      pairs.keys.push_back(std::move(ck));
-      pairs.rows.push_back(std::move(cr));
-      pairs.counts.push_back(A.n);
-      pairs.pending += A.n;
-      // many anchors contribute to the same boundary pair (theta, n = 2000:
-      // 162 M contributions, 2.5 M pairs): fold them in before they pile up
-      if (pairs.pending * (C.out.P + 1) * 8ull > mem_budget / 2) compact_pairs(C.out.P);
-    }
+    if (M.out_kind == 4) pairs.n = d2h(pairs.counter.as<uint64_t>());
   }
 
-  // Folds the pending contributions into the running pair table.
-  void compact_pairs(uint32_t P) {
-    if (pairs.pending == 0) return;
-    const uint64_t W = pairs.pending + pairs.run_n;
-    DBuf allk(W * 8), allr(std::max<uint64_t>(W * P, 1) * 8);
-    uint64_t o = 0;
-    auto put = [&](const DBuf& k, const DBuf& r, uint64_t c) {
-      if (!c) return;
-      MB_CUDA(cudaMemcpyAsync(allk.as<uint64_t>() + o, k.p, c * 8, cudaMemcpyDeviceToDevice, stream));
-      MB_CUDA(cudaMemcpyAsync(allr.as<uint64_t>() + o * P, r.p, c * P * 8, cudaMemcpyDeviceToDevice, stream));
-      o += c;
-    };
-    put(pairs.run_key, pairs.run_pay, pairs.run_n);
-    for (size_t i = 0; i < pairs.counts.size(); ++i) put(pairs.keys[i], pairs.rows[i], pairs.counts[i]);
-    pairs.keys.clear();
-    pairs.rows.clear();
-    pairs.counts.clear();
-    pairs.run_key.release();
-    pairs.run_pay.release();
-    static const bool dbg = std::getenv("MB_DEBUG_HOPS") != nullptr;
-    uint64_t nk = 0;
-    aggregate(allk, allr, W, P, pairs.run_key, pairs.run_pay, nk, 2 * bits);
-    if (dbg) fprintf(stderr, "pairs: %llu pending + %llu running -> %llu\n", (unsigned long long)pairs.pending,
-                     (unsigned long long)pairs.run_n, (unsigned long long)nk);
-    pairs.run_n = nk;
-    pairs.pending = 0;
+  // Makes room for `need` keys in the running pair table: a larger table is
+  // rebuilt from the dense (key, row) list, whose indices stay valid.
+  void reserve_pairs(uint32_t P, uint64_t need) {
+    if (need <= pairs.cap_rows && pairs.key.p) return;
+    uint64_t rows = std::max<uint64_t>(1ull << 16, pairs.cap_rows);
+    while (rows < need) rows *= 2;
+    if (need > 0xFFFFFFF0ull) fail(kBudget, "pair table exceeds 2^32 keys");
+    int lg = 1;
+    while ((1ull << lg) < 2 * rows) ++lg;
+    PairHash nh;
+    nh.cap_rows = rows;
+    nh.shift = 64 - lg;
+    nh.key.alloc((2 * rows) * 8);
+    nh.idx.alloc((2 * rows) * 4);
+    nh.list.alloc(rows * 8);
+    nh.rows.alloc(rows * P * 8);
+    nh.counter.alloc(8);
+    MB_CUDA(cudaMemsetAsync(nh.key.p, 0xFF, 2 * rows * 8, stream));
+    MB_CUDA(cudaMemsetAsync(nh.idx.p, 0xFF, 2 * rows * 4, stream));
+    MB_CUDA(cudaMemsetAsync(nh.rows.p, 0, rows * P * 8, stream));
+    nh.n = pairs.n;
+    if (pairs.key.p && pairs.n) {
+      MB_CUDA(cudaMemcpyAsync(nh.list.p, pairs.list.p, pairs.n * 8, cudaMemcpyDeviceToDevice, stream));
+      MB_CUDA(cudaMemcpyAsync(nh.rows.p, pairs.rows.p, pairs.n * P * 8, cudaMemcpyDeviceToDevice, stream));
+      launch("pair_rehash", [&] {
+        k_pair_rehash<<<grid_for(pairs.n, 256), 256, 0, stream>>>(nh.list.as<uint64_t>(), pairs.n, nh.key.as<uint64_t>(),
+                                                                  nh.idx.as<uint32_t>(), 2 * rows - 1, nh.shift);
+      });
+    }
+    MB_CUDA(cudaMemcpyAsync(nh.counter.p, &nh.n, 8, cudaMemcpyHostToDevice, stream));
+    MB_CUDA(cudaStreamSynchronize(stream));  // &nh.n is a host stack value
+    pairs = std::move(nh);
   }
 
   // Evaluates position h of Eq. 1 for anchors [x0, x0+nx); false = split and
   // retry (nothing has been accumulated for this (h, batch) yet).
+  Arena arena;  // per-batch scratch (reset at every batch)
+
   bool run_batch(const CycleDesc& C, int h, uint32_t x0, uint32_t nx) {
+    arena.top = 0;  // the previous batch's buffers are all dead (stream order keeps reuse safe)
+    ArenaScope scope(arena.base ? &arena : nullptr);
     const int L = C.L, nb = static_cast<int>(C.bpos.size());
     int d, rec = -1;
     int ks0 = 0, ks1 = 0;  // output key sources: 0 x, 1 v, 2 r
@@ -950,10 +1055,32 @@ struct CycleRunner {
           cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
         }
         const uint64_t avail = fr + (reserved > used ? reserved - used : 0) + dbuf_cache().cached;
-        mem_budget = std::min<uint64_t>(48ull << 30, std::max<uint64_t>(2ull << 30, avail / 4));
+        // a pair-keyed output also holds its pending contributions, the
+        // running table and the compaction's sort buffers outside the arena
+        const uint64_t div = C.out.kind == 4 ? 8 : 4;
+        mem_budget = std::min<uint64_t>(48ull << 30, std::max<uint64_t>(2ull << 30, avail / div));
       }
       static const char* mb_env = std::getenv("MB_CYCLE_BUDGET_MB");
       if (mb_env) mem_budget = std::strtoull(mb_env, nullptr, 10) << 20;
+    }
+    // the per-batch arena: the per-hop budget (a hop's hash table, keys and
+    // rows plus the frontiers and B parts that are still alive; a batch that
+    // needs more spills into ordinary pool allocations)
+    DBuf arena_mem;
+    {
+      static const bool no_arena = std::getenv("MB_NO_ARENA") != nullptr;
+      ArenaScope off(nullptr);
+      if (!no_arena) {
+        size_t fr = 0, tot = 0;
+        MB_CUDA(cudaMemGetInfo(&fr, &tot));
+        // one budget: a batch that needs more spills to pool allocations
+        const uint64_t want = std::min<uint64_t>(mem_budget, (static_cast<uint64_t>(fr) + dbuf_cache().cached) / 3);
+        if (want >= (64ull << 20)) {
+          arena_mem.alloc(want);
+          arena.base = arena_mem.as<char>();
+          arena.cap = want;
+        }
+      }
     }
     static const bool no_sym = std::getenv("MB_NO_CYCLE_SYMMETRY") != nullptr;
     const bool sym = rotation_symmetric(C) && !no_sym;
@@ -968,13 +1095,46 @@ struct CycleRunner {
     const auto t_solve = std::chrono::steady_clock::now();
     wait_s = 0;
     t_dbuf_alloc_s = 0;
+    // Per-anchor work estimate: S2[x] = sum of the degrees of x's suffix
+    // neighbours bounds the second hop of x's half paths.  A batch is the
+    // longest anchor range whose S2 sum times the learned ratio (bytes of the
+    // largest hop per unit of S2, from the last batches) fits the budget.
+    const std::vector<double>& pre = s2_prefix();
+    auto pick = [&](uint32_t x0, double ratio) -> uint32_t {
+      if (ratio <= 0) return std::min<uint32_t>(G.n - x0, 1024);
+      const double lim = pre[x0] + static_cast<double>(mem_budget) / ratio;
+      const uint32_t hi = static_cast<uint32_t>(std::min<uint64_t>(G.n, static_cast<uint64_t>(x0) + first_batch));
+      const uint32_t e = static_cast<uint32_t>(std::upper_bound(pre.begin() + x0 + 1, pre.begin() + hi + 1, lim) -
+                                               pre.begin()) - 1;
+      return std::max<uint32_t>(1, e - x0);
+    };
+    static const bool old_batches = std::getenv("MB_HALVING_BATCHES") != nullptr;
     for (int h = 0; h < nh; ++h) {
-      uint32_t bs = first_batch, cap = first_batch;  // cap: below the last size that failed
+      uint32_t bs = first_batch, cap = first_batch;  // (MB_HALVING_BATCHES) cap: below the last size that failed
+      double ratio = 0;  // 0: unknown yet (a first probe batch of 1024 anchors)
       for (uint32_t x0 = 0; x0 < G.n;) {
-        const uint32_t nx = std::min(bs, G.n - x0);
+        const uint32_t nx = old_batches ? std::min(bs, G.n - x0) : pick(x0, ratio);
         force = nx == 1;
-        if (run_batch(C, h, x0, nx)) {
+        batch_need = 0;
+        const bool done = run_batch(C, h, x0, nx);
+        const double s2 = std::max(1.0, pre[x0 + nx] - pre[x0]);
+        if (!done) {
+          ++failed;
+          bs = std::max<uint32_t>(1, nx / 2);
+          cap = bs;
+          // the refused hop's need, with slack; a range that cannot shrink by
+          // estimate any more is halved
+          const double r = 1.25 * static_cast<double>(last_over) / s2;
+          ratio = std::max(ratio * 2, r);
+          if (!old_batches && pick(x0, ratio) >= nx) ratio = static_cast<double>(mem_budget) / std::max(1.0, pre[x0 + std::max<uint32_t>(1, nx / 2)] - pre[x0]);
+          continue;
+        }
+        {
           ++ok;
+          // learned ratio: this batch's largest hop per unit of S2 (decaying
+          // towards the lighter anchors further along the sweep)
+          const double r = 1.25 * static_cast<double>(batch_need) / s2;
+          ratio = ratio <= 0 ? r : std::max(r, 0.7 * ratio);
           x0 += nx;
           // fail fast: every contribution is non-negative and the anchors run
           // hubs first, so once a checked add or multiply has overflowed the
@@ -989,10 +1149,6 @@ struct CycleRunner {
           // anchors get lighter along the sweep: grow, but only slowly past a failure
           cap = static_cast<uint32_t>(std::min<uint64_t>(first_batch, cap + cap / 4 + 1));
           bs = static_cast<uint32_t>(std::min<uint64_t>(2ull * nx, cap));
-        } else {
-          ++failed;
-          bs = std::max<uint32_t>(1, nx / 2);
-          cap = bs;
         }
       }
     }
@@ -1009,16 +1165,29 @@ struct CycleRunner {
   // sorted pair table with CSR rows (and the transposed copy).
   void finish_pairs(uint32_t P, DBuf& key, DBuf& pay, uint64_t& nk, DBuf& off, DBuf& cols, DBuf& off_t,
                     DBuf& cols_t, DBuf& pay_t) {
-    compact_pairs(P);
-    nk = pairs.run_n;
+    // the pair table in key order: sort the dense key list, gather the rows
+    nk = pairs.n;
+    key.alloc(std::max<uint64_t>(nk, 1) * 8);
+    pay.alloc(std::max<uint64_t>(nk * P, 1) * 8);
     if (nk) {
-      key = std::move(pairs.run_key);
-      pay = std::move(pairs.run_pay);
-    } else {
-      key.alloc(8);
-      pay.alloc(8);
+      DBuf didx(nk * 4), sidx(nk * 4);
+      launch("cycle_iota", [&] { k_iota<uint32_t><<<grid_for(nk, 256), 256, 0, stream>>>(didx.as<uint32_t>(), nk); });
+      sort_pairs(pairs.list.as<uint64_t>(), key.as<uint64_t>(), didx.as<uint32_t>(), sidx.as<uint32_t>(), nk, 2 * bits);
+      launch("pair_gather", [&] {
+        k_gather_rows32<<<grid_for(nk * P, 256), 256, 0, stream>>>(sidx.as<uint32_t>(), pairs.rows.as<uint64_t>(), P, nk,
+                                                                   pay.as<uint64_t>());
+      });
     }
-    pairs = PairBuild{};
+    {
+      static const bool dbg = std::getenv("MB_DEBUG_PAIRS") != nullptr;
+      if (dbg) {
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        fprintf(stderr, "pairs: table of %llu keys (capacity %llu; free %.1f GB, cached %.1f GB)\n",
+                (unsigned long long)nk, (unsigned long long)pairs.cap_rows, fr / 1e9, dbuf_cache().cached / 1e9);
+      }
+    }
+    pairs = PairHash{};
     build_csr(key, nk, off, cols);
     // transpose: swap the two keys, sort, gather rows
     DBuf tk(std::max<uint64_t>(nk, 1) * 8), idx(std::max<uint64_t>(nk, 1) * 8), sk(std::max<uint64_t>(nk, 1) * 8),

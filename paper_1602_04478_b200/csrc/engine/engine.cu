@@ -57,7 +57,7 @@ struct DBufCache {
   std::mutex mu;
   std::map<cudaStream_t, std::multimap<size_t, void*>> blocks;
   size_t cached = 0;
-  static constexpr size_t kCap = 64ull << 30;
+  static constexpr size_t kCap = 24ull << 30;
   static size_t round(size_t b) {
     const size_t g = b > (64ull << 20) ? (2ull << 20) : (64ull << 10);
     return (b + g - 1) / g * g;
@@ -97,28 +97,57 @@ inline DBufCache& dbuf_cache() {
   return *c;
 }
 
+// Bump arena for the cycle engine's per-batch scratch (frontiers, hash
+// tables, work offsets): one block carved up in stream order and reset per
+// anchor batch, instead of thousands of pool allocations per solve (those
+// cost up to 10 s of host time per colouring on the theta query).
+struct Arena {
+  char* base = nullptr;
+  size_t cap = 0, top = 0;
+};
+thread_local Arena* t_arena = nullptr;
+
+struct ArenaScope {  // routes non-persistent DBuf allocations of this thread to `a` (nullptr: off)
+  Arena* prev;
+  explicit ArenaScope(Arena* a) : prev(t_arena) { t_arena = a; }
+  ~ArenaScope() { t_arena = prev; }
+};
+
 struct DBuf {
   void* p = nullptr;
   size_t cap = 0;  // bytes actually allocated (size class)
   size_t bytes = 0;
   cudaStream_t s = nullptr;
   bool persistent = false;
+  bool in_arena = false;
   DBuf() = default;
   explicit DBuf(size_t b) { alloc(b); }
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept : p(o.p), cap(o.cap), bytes(o.bytes), s(o.s), persistent(o.persistent) {
-    o.p = nullptr, o.bytes = 0, o.cap = 0;
+  DBuf(DBuf&& o) noexcept
+      : p(o.p), cap(o.cap), bytes(o.bytes), s(o.s), persistent(o.persistent), in_arena(o.in_arena) {
+    o.p = nullptr, o.bytes = 0, o.cap = 0, o.in_arena = false;
   }
   DBuf& operator=(DBuf&& o) noexcept {
     release();
-    p = o.p, cap = o.cap, bytes = o.bytes, s = o.s, persistent = o.persistent;
-    o.p = nullptr, o.bytes = 0, o.cap = 0;
+    p = o.p, cap = o.cap, bytes = o.bytes, s = o.s, persistent = o.persistent, in_arena = o.in_arena;
+    o.p = nullptr, o.bytes = 0, o.cap = 0, o.in_arena = false;
     return *this;
   }
   ~DBuf() { release(); }
   void alloc(size_t b) {
     release();
+    if (b && !persistent && t_arena) {
+      const size_t r = (b + 255) & ~size_t(255);
+      if (t_arena->top + r <= t_arena->cap) {
+        p = t_arena->base + t_arena->top;
+        t_arena->top += r;
+        cap = r;
+        bytes = b;
+        in_arena = true;
+        return;
+      }
+    }
     if (b) {
       if (persistent) {
         MB_CUDA(cudaMalloc(&p, b));
@@ -131,7 +160,25 @@ struct DBuf {
         if (p) {
           cap = got;  // a cached block may be larger than asked for
         } else {
-          MB_CUDA(cudaMallocAsync(&p, cap, s));
+          cudaError_t e = cudaMallocAsync(&p, cap, s);
+          if (e == cudaErrorMemoryAllocation) {
+            // the size-class cache holds freed blocks the pool cannot hand
+            // out for other sizes: give them all back and retry once
+            (void)cudaGetLastError();  // not sticky: clear it for the next launch check
+            dbuf_cache().clear(s);
+            cudaMemPool_t pool;
+            int dev = 0;
+            if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+              cudaStreamSynchronize(s);
+              cudaMemPoolTrimTo(pool, 0);
+            }
+            e = cudaMallocAsync(&p, cap, s);
+            if (e != cudaSuccess) (void)cudaGetLastError();
+          }
+          if (e != cudaSuccess)
+            ::mb::fail(e == cudaErrorMemoryAllocation ? ::mb::kBudget : ::mb::kCuda,
+                       std::string("device allocation of ") + std::to_string(cap >> 20) + " MB: " +
+                           cudaGetErrorString(e));
         }
         t_dbuf_alloc_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
       }
@@ -139,6 +186,10 @@ struct DBuf {
     bytes = b;
   }
   void release() {
+    if (p && in_arena) {
+      p = nullptr, bytes = 0, cap = 0, in_arena = false;
+      return;
+    }
     if (p) {
       if (persistent) cudaFree(p);
       else if (!dbuf_cache().put(s, cap, p)) cudaFreeAsync(p, s);

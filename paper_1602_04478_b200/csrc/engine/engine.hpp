@@ -71,6 +71,13 @@ class GpuEngine {
   const EngineStats& stats() const;
   void* stream() const;
   int device() const;
+  // Vertex sharding: count() then returns this rank's partial
+  // count, the matches anchored at the device vertices x with
+  // x % world == rank; the partials of all ranks add up to the count.  Only a
+  // root cycle block with a scalar output is split (root_shardable());
+  // otherwise rank 0 returns the whole count and the other ranks 0.
+  void set_shard(uint32_t rank, uint32_t world);
+  bool root_shardable() const;
 
   struct Impl;
 

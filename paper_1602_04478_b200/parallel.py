@@ -96,3 +96,54 @@ def distributed_estimate(g, plan, engine: int, trials: int, seed: int, k: int | 
     seeds = [derive_seed(seed, i) for i in range(trials)]
     per = distributed_count_seeds(g, plan, seeds, engine, count_fn, device)
     return estimate_from_counts(k, edges, per)
+
+
+def sum_partials(parts: Sequence[Sequence[int]], overflowed: Sequence[bool]) -> np.ndarray:
+    """Adds the ranks' partial counts with the reference's checked u64
+    arithmetic (errors.hpp:38-50): a rank that overflowed, or a sum >= 2^64,
+    is the reference's OverflowError."""
+    from . import CountOverflowError
+
+    if any(overflowed):
+        raise CountOverflowError("count overflow (64-bit)")
+    tot = [sum(int(p[c]) for p in parts) for c in range(len(parts[0]))] if parts else []
+    if any(t >= 1 << 64 for t in tot):
+        raise CountOverflowError("count overflow in addition")
+    return np.asarray(tot, dtype=np.uint64)
+
+
+def distributed_count_vertex_sharded(g, plan, chis, engine: int = 1, count_fn: Callable | None = None,
+                                     device=None) -> np.ndarray:
+    """Counts of the colourings `chis` (c, n) with the data-graph vertices
+    sharded over the ranks: each rank sums the root-block matches anchored at
+    its vertices (mb_count_colorful_shard), and the partials are combined by
+    one all-gather + checked sum, the reference's sharded total
+    (runtime.cpp:297-302).  Every rank returns the full counts.
+    ``count_fn(rank, world) -> (partials, overflowed)`` replaces the device
+    call in the CPU tests."""
+    import torch
+
+    from . import CountOverflowError, count_colorful_shard
+
+    dist, world, rank = _world()
+    chis = np.atleast_2d(chis)
+    overflowed = False
+    if count_fn is not None:
+        part, overflowed = count_fn(rank, world)
+        part = np.asarray(part, dtype=np.uint64)
+    else:
+        try:
+            part, _ = count_colorful_shard(g, plan, chis, rank, world, engine)
+        except CountOverflowError:
+            part, overflowed = np.zeros(len(chis), np.uint64), True
+    if world == 1:
+        return sum_partials([part], [overflowed])
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else "cpu"
+    buf = torch.zeros(len(chis) + 1, dtype=torch.int64, device=device)
+    buf[: len(chis)] = torch.from_numpy(part.astype(np.uint64).view(np.int64)).to(device)
+    buf[len(chis)] = 1 if overflowed else 0
+    gathered = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(gathered, buf)
+    rows = [t.cpu().numpy().view(np.uint64) for t in gathered]
+    return sum_partials([r[:-1] for r in rows], [bool(r[-1]) for r in rows])

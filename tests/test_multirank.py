@@ -86,3 +86,58 @@ def test_two_ranks_gloo_estimate_matches_reference():
             assert mean == e["mean"]
             assert cv == e["cv"]
             assert sub == e["subgraph"]
+
+
+def _shard_worker(rank, world, port, results):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1602_04478_b200 import CountOverflowError, parallel
+        from oracle import Oracle
+
+        O = Oracle()
+        gold = json.load(open(os.path.join(ROOT, "tests", "golden", "counts.json")))
+        g = gold["graphs"]["skew60"]
+        off, adj, _ = O.build_csr(g["n"], g["edges"])
+        c5 = [(0, 1), (1, 2), (2, 3), (3, 4), (4, 0)]
+        chis = [O.random_coloring(g["n"], 5, s) for s in (1, 2)]
+        want = [O.brute(off, adj, 5, c5, c) for c in chis]
+
+        # each rank reports an uneven share of every colouring's count
+        def fn(r, w):
+            return [(x // 3 if r == 0 else x - x // 3) for x in want], False
+
+        got = parallel.distributed_count_vertex_sharded(None, None, np.stack(chis), count_fn=fn, device="cpu")
+        # partials whose sum passes 2^64 are the reference's OverflowError on every rank
+        big = lambda r, w: ([(1 << 63) + 5], False)
+        try:
+            parallel.distributed_count_vertex_sharded(None, None, np.stack(chis[:1]), count_fn=big, device="cpu")
+            over = "none"
+        except CountOverflowError:
+            over = "sum"
+        # one rank overflowing alone is an overflow everywhere
+        one = lambda r, w: ([0], r == 1)
+        try:
+            parallel.distributed_count_vertex_sharded(None, None, np.stack(chis[:1]), count_fn=one, device="cpu")
+            over1 = "none"
+        except CountOverflowError:
+            over1 = "rank"
+        results[rank] = ([int(x) for x in got], want, over, over1)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_ranks_gloo_vertex_sharded_sum():
+    """Vertex-sharded counting plumbing (parallel.distributed_count_vertex_sharded):
+    the ranks' partial counts are all-gathered and added with checked u64
+    arithmetic; overflow on any rank or in the sum raises on every rank."""
+    mgr = mp.Manager()
+    results = mgr.dict()
+    mp.spawn(_shard_worker, args=(2, _free_port(), results), nprocs=2, join=True)
+    for rank in (0, 1):
+        got, want, over, over1 = results[rank]
+        assert got == want
+        assert over == "sum" and over1 == "rank"

@@ -79,7 +79,12 @@ def main():
         traffic[label] = {"dram_bytes_per_launch": dram, "source": f"profiles/{tag}_ncu_full_summary.txt"}
     text = "\n".join(lines) + "\n"
     open(f"profiles/{tag}_ncu_full_summary.txt", "w").write(text)
-    json.dump(traffic, open("profiles/ncu_traffic.json", "w"), indent=1)
+    try:  # merge: other kernels' entries (other configs' captures) stay
+        merged = json.load(open("profiles/ncu_traffic.json"))
+    except (OSError, ValueError):
+        merged = {}
+    merged.update(traffic)
+    json.dump(merged, open("profiles/ncu_traffic.json", "w"), indent=1)
     print(text)
 
 

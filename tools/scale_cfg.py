@@ -17,6 +17,11 @@ for sz in sys.argv[2:]:
     plan = mb.QueryPlan(cfg["k"], cfg["query"])
     chi = np.stack([mb.random_coloring(g, cfg["k"], s) for s in cfg["seeds"][:1]])
     t = time.time()
+    import os
+    if os.environ.get("MB_TIMING"):
+        mb.count_colorful(g, plan, mb.random_coloring(g, cfg["k"], 1))  # warm: upload + indexes
+        mb.engine_enable_timing(g, True)
+        t = time.time()
     try:
         c = mb.count_colorful(g, plan, chi)
         dt = time.time() - t
@@ -25,4 +30,8 @@ for sz in sys.argv[2:]:
               mb.engine_stats(g), flush=True)
     except Exception as e:
         print(f"size {sz} n={g.num_vertices()} m={g.num_edges()} FAILED after {time.time()-t:.1f}s: {e}", flush=True)
+    if os.environ.get("MB_TIMING"):
+        for name, ms, n, b in sorted(mb.engine_timings(g), key=lambda t: -t[1])[:12]:
+            print(f"   {name:28s} {ms:10.2f} ms  {n:7d} launches  {b / max(ms, 1e-9) / 1e6:8.1f} GB/s", flush=True)
+        mb.engine_enable_timing(g, False)
         continue
