@@ -240,6 +240,8 @@ template <bool KEYS>
 __global__ void __launch_bounds__(kHopTile) k_hop_expand(HopArgs A) {
   __shared__ uint64_t s_woff[kHopTile + 1];
   __shared__ uint64_t s_e0, s_cnt;
+  __shared__ uint32_t s_binom[KEYS ? 1 : (kMaxColors + 1) * kBinomStride];
+  if (!KEYS) stage_binom(c_lut, s_binom);
   const uint64_t item0 = static_cast<uint64_t>(blockIdx.x) * kHopTile;
   const uint64_t item = item0 + threadIdx.x;
   auto entry_of = [&](uint64_t it) {  // last i with woff[i] <= it
@@ -355,7 +357,7 @@ __global__ void __launch_bounds__(kHopTile) k_hop_expand(HopArgs A) {
           S2 = S1;
           v2 = v1;
         }
-        const uint32_t o = sig_index(c_lut, S2, fout);
+        const uint32_t o = sig_index_sm(s_binom, S2, fout);
         if (o >= A.P_out || mb_popc(S2) != A.s_out) {
           atomicOr(A.err, 16);  // signature outside the frontier row: plan/popcount bug
           continue;
@@ -460,6 +462,9 @@ __device__ __forceinline__ uint64_t find_slot(const GraphView& G, uint32_t p, ui
 }
 
 __global__ void __launch_bounds__(256) k_half_merge(MergeArgs A) {
+  __shared__ uint32_t s_binom[(kMaxColors + 1) * kBinomStride];
+  stage_binom(c_lut, s_binom);
+  __syncthreads();
   const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   uint64_t local = 0, upd = 0;
   if (i < A.nA) {
@@ -516,9 +521,9 @@ __global__ void __launch_bounds__(256) k_half_merge(MergeArgs A) {
           if (A.out_kind == 1) {
             local = add_ck(local, val, A.err);
           } else if (A.out_kind == 4) {
-            atomic_add_ck(reinterpret_cast<u64*>(A.ph_rows + orow + sig_index(c_lut, Sa | Sb, ofix)), val, A.err);
+            atomic_add_ck(reinterpret_cast<u64*>(A.ph_rows + orow + sig_index_sm(s_binom, Sa | Sb, ofix)), val, A.err);
           } else {
-            atomic_add_ck(reinterpret_cast<u64*>(A.out + orow + sig_index(c_lut, Sa | Sb, ofix)), val, A.err);
+            atomic_add_ck(reinterpret_cast<u64*>(A.out + orow + sig_index_sm(s_binom, Sa | Sb, ofix)), val, A.err);
           }
         }
       }

@@ -91,6 +91,28 @@ MB_HD uint32_t sig_rank(const SigLut& L, uint32_t m) {
 __device__ __forceinline__ uint32_t sig_unrank(const SigLut& L, int t, uint32_t r) {
   return __ldg(L.unrank + L.off[t] + r);
 }
+
+// Shared-memory copy of the binomial table for kernels whose lanes rank
+// different masks at once: indexing __constant__ memory with lane-divergent
+// addresses serialises the warp, a shared-memory lookup does not.
+constexpr int kBinomStride = kMaxColors + 2;
+__device__ __forceinline__ void stage_binom(const SigLut& L, uint32_t* sb) {
+  for (int i = threadIdx.x; i < (kMaxColors + 1) * kBinomStride; i += blockDim.x)
+    sb[i] = L.binom[i / kBinomStride][i % kBinomStride];
+}
+__device__ __forceinline__ uint32_t sig_rank_sm(const uint32_t* sb, uint32_t m) {
+  uint32_t r = 0;
+  int i = 1;
+  while (m) {
+    const int c = __ffs(m) - 1;
+    m &= m - 1u;
+    r += sb[c * kBinomStride + i++];
+  }
+  return r;
+}
+__device__ __forceinline__ uint32_t sig_index_sm(const uint32_t* sb, uint32_t m, uint32_t fixed) {
+  return sig_rank_sm(sb, sig_compress(m & ~fixed, fixed));
+}
 #endif
 
 // Payload index of the full signature m in a row whose fixed colours are `fixed`.
