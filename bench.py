@@ -162,8 +162,8 @@ def dist_setup(args):
 
 def ref_layout(nc):
     """Host-thread layout for the reference: one colouring per thread (as its
-    estimate() does, estimate.cpp:149), spare cores given to each colouring as
-    BSP workers (parallel_count, runtime.cpp:311).  Measured on the 16-core GPU
+    estimate() does, estimate.cpp:108-117), spare cores given to each colouring as
+    BSP workers (parallel_count, runtime.cpp:311-324).  Measured on the 16-core GPU
     host at the config-1 sample: 8x1 0.60, 1x16 0.42, 8x2 0.69, 4x4 0.61 col/s."""
     ncpu = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
     threads = max(1, min(ncpu, nc))

@@ -60,7 +60,7 @@ int mb_graph_validate(const mb_graph* g);
 
 /* random_coloring (graph.hpp:85): chi[v] in 1..k, std::mt19937_64(seed). */
 int mb_random_coloring(uint32_t n, int k, uint64_t seed, uint8_t* chi);
-/* derive_seed (rng.hpp:105): per-trial seed stream of estimate(). */
+/* derive_seed (rng.hpp:18): per-trial seed stream of estimate(). */
 uint64_t mb_derive_seed(uint64_t master, uint64_t stream);
 
 /* ---- query and plan (include/motif/query.hpp) ------------------------------ */
@@ -74,7 +74,7 @@ void mb_plan_free(mb_plan* p);
 int mb_plan_k(const mb_plan* p);
 int mb_plan_num_trees(const mb_plan* p);
 /* Index of the tree select_plan chose; mb_plan_use_tree switches the tree
- * the counting calls run (plan-invariance checks, engine_test.cpp:343). */
+ * the counting calls run (plan-invariance checks, tests/test_engine.cpp:187-200). */
 int mb_plan_selected(const mb_plan* p);
 int mb_plan_use_tree(mb_plan* p, int idx);
 /* DecompositionTree::canonical (query.hpp:76) of tree idx (-1 = in use). */

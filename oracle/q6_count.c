@@ -6,7 +6,7 @@
  * Query q6 (BASELINE.json configs[1]): edges 0-1, 1-2, 2-0, 1-3, 3-2, 2-4,
  * 4-5 — two triangles sharing the edge 1-2 and the path 2-4-5; k = 6.  A
  * colourful match is an injective image with six distinct colours, counted
- * labelled, as the reference's count_colorful counts them (engine.cpp:271-280;
+ * labelled, as the reference's count_colorful counts them (engine.cpp:265-280;
  * C3 on K3 = 6 in tests/test_engine.cpp).  Derived from the reference's join
  * rules, not from the GPU kernels:
  *   - the two triangles are the common neighbours w0, w3 of the edge a -> b

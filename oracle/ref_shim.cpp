@@ -167,8 +167,8 @@ int ref_count_colorful(void* gp, const uint8_t* chi, int k, void* pp, int tree_i
 
 // count_colorful for `nc` colourings (n bytes each) on up to `threads` host
 // threads, one colouring per thread at a time (workers > 1: each colouring
-// through parallel_count's BSP executor, runtime.cpp:311) (the reference's estimate()
-// parallelises the same way, estimate.cpp:149).  Returns the first error.
+// through parallel_count's BSP executor, runtime.cpp:311-324) (the reference's estimate()
+// parallelises the same way, estimate.cpp:108-117).  Returns the first error.
 int ref_count_batch(void* gp, const uint8_t* chis, int nc, int k, void* pp, int engine, int threads,
                     int workers, uint64_t* out) {
   auto* rg = static_cast<RefGraph*>(gp);

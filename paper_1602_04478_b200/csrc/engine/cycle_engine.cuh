@@ -1,7 +1,7 @@
 // General cycle-block solver (any length L >= 3, any node/edge annotations,
 // 0/1/2 boundary nodes).  Included by engine.cu after its helpers.
 //
-// Degree-based (DB) evaluation, reference engine.cpp:337-366 and paper §5.1
+// Degree-based (DB) evaluation, reference engine.cpp:212-241 and paper §5.1
 // Eq. 1: every labelled match of the cycle has exactly one position h holding
 // its (degree, id)-highest vertex x.  For each h the cycle is split into two
 // half paths that start at x and meet at a position d; every other image must
@@ -507,23 +507,45 @@ __global__ void __launch_bounds__(256) k_half_merge(MergeArgs A) {
       const uint64_t* ra = A.payA + i * A.PA;
       const uint64_t* rb = A.payB + lo * A.PB;
       const int ta = A.sA - 2, tb = A.sB - 2;
+      // B's nonzero entries with their colour sets, once per A entry (not once
+      // per (A entry, A signature)); rows wider than kMergeB take the plain loop
+      constexpr uint32_t kMergeB = 32;
+      uint32_t sbl[kMergeB];
+      uint64_t vbl[kMergeB];
+      uint32_t nbl = 0;
+      const bool listed = A.PB <= kMergeB;
+      if (listed)
+        for (uint32_t ib = 0; ib < A.PB; ++ib) {
+          const uint64_t vb = rb[ib];
+          if (!vb) continue;
+          sbl[nbl] = sig_expand(sig_unrank(c_lut, tb, ib), f2);
+          vbl[nbl++] = vb;
+        }
+      auto term = [&](uint32_t Sa, uint64_t va, uint32_t Sb, uint64_t vb) {
+        if ((Sa & Sb) != f2) return;
+        // a term standing for several equal Eq. 1 terms (reflection
+        // symmetry, CycleRunner::solve) is counted that many times
+        const uint64_t val = A.out_kind == 1 || A.scalar_mult == 1 ? mul_ck(va, vb, A.err)
+                                                                   : mul_ck(mul_ck(va, vb, A.err), A.scalar_mult, A.err);
+        ++upd;
+        if (A.out_kind == 1) {
+          local = add_ck(local, val, A.err);
+        } else if (A.out_kind == 4) {
+          atomic_add_ck(reinterpret_cast<u64*>(A.ph_rows + orow + sig_index_sm(s_binom, Sa | Sb, ofix)), val, A.err);
+        } else {
+          atomic_add_ck(reinterpret_cast<u64*>(A.out + orow + sig_index_sm(s_binom, Sa | Sb, ofix)), val, A.err);
+        }
+      };
       for (uint32_t ia = 0; ia < A.PA; ++ia) {
         const uint64_t va = ra[ia];
         if (!va) continue;
         const uint32_t Sa = sig_expand(sig_unrank(c_lut, ta, ia), f2);
-        for (uint32_t ib = 0; ib < A.PB; ++ib) {
-          const uint64_t vb = rb[ib];
-          if (!vb) continue;
-          const uint32_t Sb = sig_expand(sig_unrank(c_lut, tb, ib), f2);
-          if ((Sa & Sb) != f2) continue;
-          const uint64_t val = mul_ck(va, vb, A.err);
-          ++upd;
-          if (A.out_kind == 1) {
-            local = add_ck(local, val, A.err);
-          } else if (A.out_kind == 4) {
-            atomic_add_ck(reinterpret_cast<u64*>(A.ph_rows + orow + sig_index_sm(s_binom, Sa | Sb, ofix)), val, A.err);
-          } else {
-            atomic_add_ck(reinterpret_cast<u64*>(A.out + orow + sig_index_sm(s_binom, Sa | Sb, ofix)), val, A.err);
+        if (listed) {
+          for (uint32_t j = 0; j < nbl; ++j) term(Sa, va, sbl[j], vbl[j]);
+        } else {
+          for (uint32_t ib = 0; ib < A.PB; ++ib) {
+            const uint64_t vb = rb[ib];
+            if (vb) term(Sa, va, sig_expand(sig_unrank(c_lut, tb, ib), f2), vb);
           }
         }
       }
@@ -685,7 +707,7 @@ struct CycleRunner {
   }
 
   // Sort contributions (keys[W], rows[W][P]) and add equal keys: the
-  // reference's hash-map accumulate (table.cpp:190) as sort + segmented add.
+  // reference's hash-map accumulate (table.cpp:38-54) as sort + segmented add.
   // Keys equal to UINT64_MAX are dropped.  Valid keys are below 2^key_bits;
   // sorting key_bits + 1 bits keeps the sentinel (that bit set) after them.
   void aggregate(const DBuf& keys, const DBuf& rows, uint64_t W, uint32_t P, DBuf& out_key, DBuf& out_pay,
@@ -1037,6 +1059,19 @@ struct CycleRunner {
   // rotation maps the labelled matches whose highest vertex sits at position h
   // one-to-one onto those with it at h + 1, so all L terms of Eq. 1 are equal
   // and the h = 0 term times L is exact (configs 0 and 2).
+  // A cycle block without annotations whose boundary positions are all fixed
+  // by one reflection p -> c2 - p (mod L): one boundary node b (c2 = 2b), or
+  // two opposite ones b0, b1 = b0 + L/2 (c2 = 2 b0; the theta's 6-cycle block
+  // keyed by (0, 7)).  Returns c2, or -1.
+  static int reflection_axis(const CycleDesc& C) {
+    for (int q = 0; q < C.L; ++q)
+      if (C.node[q].kind || C.edge[q].kind) return -1;
+    if (C.bpos.size() == 1) return (2 * C.bpos[0]) % C.L;
+    if (C.bpos.size() == 2 && C.L % 2 == 0 && ((C.bpos[1] - C.bpos[0] + C.L) % C.L) == C.L / 2)
+      return (2 * C.bpos[0]) % C.L;
+    return -1;
+  }
+
   static bool rotation_symmetric(const CycleDesc& C) {
     if (!C.bpos.empty() || C.out.kind != 1) return false;
     for (int q = 0; q < C.L; ++q)
@@ -1088,9 +1123,24 @@ struct CycleRunner {
       }
     }
     static const bool no_sym = std::getenv("MB_NO_CYCLE_SYMMETRY") != nullptr;
-    const bool sym = rotation_symmetric(C) && !no_sym;
-    h_mult = sym ? static_cast<uint32_t>(C.L) : 1u;
-    const int nh = sym ? 1 : C.L;
+    // Eq. 1 positions to evaluate, each with the number of equal terms it stands for
+    std::vector<std::pair<int, uint32_t>> hs;
+    if (rotation_symmetric(C) && !no_sym) {
+      hs.push_back({0, static_cast<uint32_t>(C.L)});
+    } else if (int c2 = reflection_axis(C); c2 >= 0 && !no_sym) {
+      // a reflection p -> c2 - p (mod L) fixes the boundary positions and
+      // maps the labelled matches whose highest vertex sits at h one-to-one
+      // onto those with it at the mirrored position, keys and colour sets
+      // unchanged: evaluate one position of each mirrored pair, twice
+      for (int h = 0; h < C.L; ++h) {
+        const int m = ((c2 - h) % C.L + C.L) % C.L;
+        if (m == h) hs.push_back({h, 1u});
+        else if (h < m) hs.push_back({h, 2u});
+      }
+    } else {
+      for (int h = 0; h < C.L; ++h) hs.push_back({h, 1u});
+    }
+    const int nh = static_cast<int>(hs.size());
     // Anchors are swept in device order (hubs first) with an adaptive batch:
     // halved when a hop would exceed the scratch budget (the attempt is
     // discarded), doubled after a success, so heavy anchors run in small
@@ -1114,7 +1164,9 @@ struct CycleRunner {
       return std::max<uint32_t>(1, e - x0);
     };
     static const bool old_batches = std::getenv("MB_HALVING_BATCHES") != nullptr;
-    for (int h = 0; h < nh; ++h) {
+    for (int hi = 0; hi < nh; ++hi) {
+      const int h = hs[hi].first;
+      h_mult = hs[hi].second;
       uint32_t bs = first_batch, cap = first_batch;  // (MB_HALVING_BATCHES) cap: below the last size that failed
       double ratio = 0;  // 0: unknown yet (a first probe batch of 1024 anchors)
       for (uint32_t x0 = 0; x0 < G.n;) {

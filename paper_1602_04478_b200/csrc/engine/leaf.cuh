@@ -1,7 +1,7 @@
 // Leaf blocks, table-driven and colouring-batched.  Included by engine.cu.
 //
 // Path-table extension along CSR rows (paper §5.2 leaf blocks; reference
-// engine.cpp:368-382: edge table -> node join on the leaf -> node join on the
+// engine.cpp:243-257: edge table -> node join on the leaf -> node join on the
 // boundary -> projection to the boundary).  For a boundary vertex x the leaf
 // side contributes, for every neighbour y, the row U_b[y] shifted by x's
 // colour.  Which output colour-set index an entry (colour of x, colour of y,

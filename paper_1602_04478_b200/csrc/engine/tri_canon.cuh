@@ -29,7 +29,7 @@
 // the scan, 4 the factor gathers.
 //
 // Reference semantics: the same 3-cycle block evaluation by DB as
-// tri_hist_kernel (engine.cpp:353-366, table.cpp:255-476 for the joins).
+// tri_hist_kernel (engine.cpp:212-241, table.cpp:135-284 for the joins).
 
 namespace canon {
 

@@ -138,7 +138,7 @@ void CsrGraph::validate() const {
   if (deg_sum != 2 * m) fail(kSpec, "degree sum != 2m");
 }
 
-// Same grammar and error text as the reference loader (graph.cpp:251-291).
+// Same grammar and error text as the reference loader (graph.cpp:65-111).
 CsrGraph load_edge_list(std::istream& in, LoadStats* st) {
   std::vector<std::pair<uint32_t, uint32_t>> edges;
   uint32_t max_id = 0;

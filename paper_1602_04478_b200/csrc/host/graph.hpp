@@ -29,7 +29,7 @@ struct CsrGraph {
   std::vector<uint64_t> offsets;  // n + 1
   std::vector<uint32_t> adj;      // 2m, sorted per row
 
-  // Orients, sorts, dedupes and drops self loops (graph.cpp:200 semantics).
+  // Orients, sorts, dedupes and drops self loops (graph.cpp:14-44 semantics).
   // `edges` holds (u,v) pairs; it is consumed.
   static CsrGraph from_edges(uint32_t n, std::vector<std::pair<uint32_t, uint32_t>>& edges,
                              LoadStats* st = nullptr);

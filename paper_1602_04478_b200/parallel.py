@@ -8,7 +8,7 @@ Two shardings, both without a data-path collective:
   whole graph resident, and the per-colouring counts are all-gathered once at
   the end (NCCL on GPUs, gloo on CPU).  This is the layout for plans whose
   tables fit one GPU (configs 0 and 1) and for estimate()'s independent trials
-  (estimate.cpp:149).
+  (estimate.cpp:108-117).
 * vertices (``distributed_count_vertex_sharded``): one colouring's root block
   is split by anchor vertex, the data-graph vertices being dealt to ranks as
   the reference's Partition deals them to BSP workers (runtime.cpp:11-25, here

@@ -7,7 +7,7 @@ enough to commit:
   plans.json      canonical serialisation of every decomposition tree and of
                   the selected plan, plus plan scores, for a set of queries
                   (reference enumerate_trees / select_plan, query.cpp)
-  colorings.json  reference random_coloring outputs (graph.cpp:328)
+  colorings.json  reference random_coloring outputs (graph.cpp:142-151)
   counts.json     explicit small edge lists (seeded generators, frozen here as
                   edge lists), colouring seeds and the reference engine's
                   colourful counts (PS and DB, engine.cpp) for several queries
