@@ -127,7 +127,8 @@ __device__ __forceinline__ void ht_insert(uint64_t* ht_key, uint32_t* ht_idx, ui
 // that finds the key before its inserter has published the index waits for
 // it (ht_idx starts as all ~0u).
 __device__ __forceinline__ uint32_t ht_get(uint64_t* ht_key, uint32_t* ht_idx, uint64_t mask, int shift, uint64_t key,
-                                           unsigned long long* n_keys, uint64_t* key_out) {
+                                           unsigned long long* n_keys, uint64_t* key_out, uint64_t* rows = nullptr,
+                                           uint32_t P = 0) {
   uint64_t h = ht_slot(key, shift);
   while (true) {
     uint64_t cur = *reinterpret_cast<volatile uint64_t*>(ht_key + h);
@@ -136,6 +137,8 @@ __device__ __forceinline__ uint32_t ht_get(uint64_t* ht_key, uint32_t* ht_idx, u
       if (cur == kEmptyKey) {
         const uint32_t idx = static_cast<uint32_t>(atomicAdd(n_keys, 1ull));
         key_out[idx] = key;
+        if (rows)
+          for (uint32_t j = 0; j < P; ++j) rows[static_cast<uint64_t>(idx) * P + j] = 0;
         __threadfence();
         atomicExch(ht_idx + h, idx);
         return idx;
@@ -236,8 +239,11 @@ constexpr int kHopTile = 256;  // items per CTA of k_hop_expand
 // materialising a row per item or sorting: aggregation costs one probe plus
 // the row atomics of the nonzero contributions.  The CTA locates its items'
 // entries once: the woff span of its tile is staged in shared memory.
-template <bool KEYS>
+// MODE 0: keys pass, 1: accumulate pass (find), 2: one fused pass (insert or
+// find, the inserter zeroes the row before publishing its index).
+template <int MODE>
 __global__ void __launch_bounds__(kHopTile) k_hop_expand(HopArgs A) {
+  constexpr bool KEYS = MODE == 0;
   __shared__ uint64_t s_woff[kHopTile + 1];
   __shared__ uint64_t s_e0, s_cnt;
   __shared__ uint32_t s_binom[KEYS ? 1 : (kMaxColors + 1) * kBinomStride];
@@ -279,17 +285,17 @@ __global__ void __launch_bounds__(kHopTile) k_hop_expand(HopArgs A) {
   uint32_t x, v, r;
   unpack_key(A.key_in[i], A.in_has_r, A.bits, x, v, r);
   if (x >= A.G.n || v >= A.G.n) {
-    if (KEYS) atomicOr(A.err, 32);
+    if (MODE != 1) atomicOr(A.err, 32);
     return;
   }
   const uint64_t slot = A.sstart[i] + (item - A.woff[i]);
   if (slot >= A.roff[A.G.n]) {
-    if (KEYS) atomicOr(A.err, 64);
+    if (MODE != 1) atomicOr(A.err, 64);
     return;
   }
   const uint32_t w = A.radj[slot];
   if (w >= A.G.n) {
-    if (KEYS) atomicOr(A.err, 128);
+    if (MODE != 1) atomicOr(A.err, 128);
     return;
   }
   if (!(A.G.ordered || A.G.rank[w] < A.G.rank[x])) return;
@@ -303,7 +309,9 @@ __global__ void __launch_bounds__(kHopTile) k_hop_expand(HopArgs A) {
     ht_insert(A.ht_key, A.ht_idx, A.ht_mask, A.ht_shift, key, A.n_keys, A.key_out);
     return;
   }
-  const uint32_t oi = ht_find(A.ht_key, A.ht_idx, A.ht_mask, A.ht_shift, key);
+  const uint32_t oi = MODE == 2 ? ht_get(A.ht_key, A.ht_idx, A.ht_mask, A.ht_shift, key, A.n_keys, A.key_out,
+                                          A.row_out, A.P_out)
+                                  : ht_find(A.ht_key, A.ht_idx, A.ht_mask, A.ht_shift, key);
   if (oi == ~0u) {
     atomicOr(A.err, 64);
     return;
@@ -809,15 +817,27 @@ struct CycleRunner {
     // (8-byte key) per pass; per input entry its key, work offsets and row;
     // per output key its slot and row
     const uint64_t hop_bytes = W * (4 + 1 + 2 * 8) + in.n * (8 + 16 + 8ull * in.P);
-    launch("cycle_hop_keys", [&] { k_hop_expand<true><<<grid_for(W, kHopTile), kHopTile, 0, stream>>>(A); },
-           hop_bytes / 2);
-    out.n = d2h(nk.as<uint64_t>());
-    out.pay.alloc(std::max<uint64_t>(out.n * out.P, 1) * 8);
-    if (out.n) MB_CUDA(cudaMemsetAsync(out.pay.p, 0, out.n * out.P * 8, stream));
-    A.row_out = out.pay.as<uint64_t>();
-    if (out.n)
-      launch("cycle_hop_expand", [&] { k_hop_expand<false><<<grid_for(W, kHopTile), kHopTile, 0, stream>>>(A); },
-             hop_bytes / 2 + out.n * (8 + 8ull * out.P));
+    static const bool two_pass = std::getenv("MB_TWO_PASS_HOPS") != nullptr;
+    if (two_pass) {
+      launch("cycle_hop_keys", [&] { k_hop_expand<0><<<grid_for(W, kHopTile), kHopTile, 0, stream>>>(A); },
+             hop_bytes / 2);
+      out.n = d2h(nk.as<uint64_t>());
+      out.pay.alloc(std::max<uint64_t>(out.n * out.P, 1) * 8);
+      if (out.n) MB_CUDA(cudaMemsetAsync(out.pay.p, 0, out.n * out.P * 8, stream));
+      A.row_out = out.pay.as<uint64_t>();
+      if (out.n)
+        launch("cycle_hop_expand", [&] { k_hop_expand<1><<<grid_for(W, kHopTile), kHopTile, 0, stream>>>(A); },
+               hop_bytes / 2 + out.n * (8 + 8ull * out.P));
+    } else {
+      // one pass: rows for at most W keys (each item adds one key at most);
+      // ht_idx starts all-ones so finders wait for the inserter's index
+      MB_CUDA(cudaMemsetAsync(out.ht_idx.p, 0xFF, cap * 4, stream));
+      out.pay.alloc(std::max<uint64_t>(W * out.P, 1) * 8);
+      A.row_out = out.pay.as<uint64_t>();
+      launch("cycle_hop_expand", [&] { k_hop_expand<2><<<grid_for(W, kHopTile), kHopTile, 0, stream>>>(A); },
+             hop_bytes);
+      out.n = d2h(nk.as<uint64_t>());
+    }
     if (dbg)
       fprintf(stderr, "hop n_in=%llu W=%llu keys=%llu s_in=%d P_in=%u first=%d in_r=%d out_r=%d rec=%d s_out=%d "
               "P_out=%u etab=%p Pe=%u ntab=%p Pn=%u bits=%d\n",
