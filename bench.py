@@ -133,6 +133,16 @@ def measured_peaks() -> dict:
     return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
+def committed_limits(kernel: str):
+    """ncu unit utilisations of the dominant kernel (profiles/r02_*_limits.json):
+    which unit binds it when HBM does not."""
+    p = os.path.join(ROOT, "profiles", f"r02_{kernel}_limits.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        return json.load(f)
+
+
 def committed_traffic(kernel: str):
     """DRAM bytes per launch of `kernel` from the committed ncu --set full summary."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -444,7 +454,7 @@ def our_arm(args, cfg, ws, rank, local):
                      "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": committed_traffic(top[0]),
                      "algorithmic_bytes_per_launch": per_launch_bytes, "launch_ms": per_launch_ms,
                      "share_of_dp_time": top[1] / total_dp_ms if total_dp_ms else None,
-                     "peak_source": peaks["source"]},
+                     "peak_source": peaks["source"], "ncu_limits": committed_limits(top[0])},
         "dp_table_updates_per_sec": stats["dp_updates"] / (ms_max / 1e3) * ws,
         "kernels": {t[0]: {"ms_per_step": t[1], "launches": t[2], "bytes": t[3]} for t in timings},
         "clocks": clk,
@@ -483,6 +493,8 @@ def main():
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sample-n", type=int, default=None,
+                    help="size of the bounded sample the reference (and the same-input GPU run) is timed on")
     ap.add_argument("--overflow-colorings", type=int, default=4,
                     help="colourings resolved per step on workloads whose count overflows u64 (configs 2, 4)")
     ap.add_argument("--size", type=int, default=None,
@@ -490,6 +502,8 @@ def main():
                          "configs 2-4, whose full sizes exceed u64 counts or HBM (DESIGN.md)")
     args = ap.parse_args()
     cfg = dict(CONFIGS[args.config], id=args.config)
+    if args.sample_n:
+        cfg["sample_n"] = args.sample_n
     ws, rank, local = dist_setup(args)
     try:
         if args.impl == "reference":

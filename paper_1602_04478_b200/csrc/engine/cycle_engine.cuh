@@ -456,6 +456,7 @@ struct MergeArgs {
   uint32_t Pout, rso;
   u64* scalar;
   uint32_t scalar_mult;  // rotation-symmetric root cycle: the h = 0 count times L
+  uint32_t t_mult;       // pair outputs: also add the contribution this many times at the swapped key
   int* err;
   u64* updates;
 };
@@ -482,7 +483,7 @@ __global__ void __launch_bounds__(256) k_half_merge(MergeArgs A) {
     const uint32_t bi = A.nB ? ht_find(A.htB_key, A.htB_idx, A.htB_mask, A.htB_shift, kb) : ~0u;
     const uint64_t lo = bi;
     bool found = bi != ~0u;
-    uint64_t orow = 0;
+    uint64_t orow = 0, orow_t = 0;
     uint32_t ofix = 0;
     const uint32_t ids[3] = {x, v, r};
     if (found && A.out_kind == 3) {
@@ -510,6 +511,11 @@ __global__ void __launch_bounds__(256) k_half_merge(MergeArgs A) {
         const uint64_t key = (static_cast<uint64_t>(p) << A.bits) | q;
         const uint32_t di = ht_get(A.ph_key, A.ph_idx, A.ph_mask, A.ph_shift, key, A.ph_n, A.ph_list);
         orow = static_cast<uint64_t>(di) * A.Pout;
+        if (A.t_mult) {
+          const uint64_t kt = (static_cast<uint64_t>(q) << A.bits) | p;
+          orow_t = static_cast<uint64_t>(ht_get(A.ph_key, A.ph_idx, A.ph_mask, A.ph_shift, kt, A.ph_n, A.ph_list)) *
+                   A.Pout;
+        }
         ofix = (1u << vcol(A.G, p)) | (1u << vcol(A.G, q));
       }
       const uint64_t* ra = A.payA + i * A.PA;
@@ -539,7 +545,11 @@ __global__ void __launch_bounds__(256) k_half_merge(MergeArgs A) {
         if (A.out_kind == 1) {
           local = add_ck(local, val, A.err);
         } else if (A.out_kind == 4) {
-          atomic_add_ck(reinterpret_cast<u64*>(A.ph_rows + orow + sig_index_sm(s_binom, Sa | Sb, ofix)), val, A.err);
+          const uint32_t o = sig_index_sm(s_binom, Sa | Sb, ofix);
+          atomic_add_ck(reinterpret_cast<u64*>(A.ph_rows + orow + o), val, A.err);
+          if (A.t_mult)
+            atomic_add_ck(reinterpret_cast<u64*>(A.ph_rows + orow_t + o),
+                          A.t_mult == A.scalar_mult ? val : mul_ck(mul_ck(va, vb, A.err), A.t_mult, A.err), A.err);
         } else {
           atomic_add_ck(reinterpret_cast<u64*>(A.out + orow + sig_index_sm(s_binom, Sa | Sb, ofix)), val, A.err);
         }
@@ -672,6 +682,11 @@ struct CycleRunner {
   uint64_t mem_budget = 6ull << 30;  // bytes of per-hop scratch per batch
   bool force = false;                 // single-anchor batch: no further split
   uint32_t h_mult = 1;                // Eq. 1 terms represented by each evaluated h
+  uint32_t h_mult_t = 0;              // ... and terms equal to it with the pair keys swapped
+  static bool no_swap_sym() {
+    static const bool off = std::getenv("MB_NO_SWAP_SYMMETRY") != nullptr;
+    return off;
+  }
   PairHash pairs;
   // pair-table streaming (engine_host.inc, streamed_root_of): called with a
   // full running table; it builds the partial table, evaluates the root on it
@@ -817,8 +832,11 @@ struct CycleRunner {
     // (8-byte key) per pass; per input entry its key, work offsets and row;
     // per output key its slot and row
     const uint64_t hop_bytes = W * (4 + 1 + 2 * 8) + in.n * (8 + 16 + 8ull * in.P);
-    static const bool two_pass = std::getenv("MB_TWO_PASS_HOPS") != nullptr;
-    if (two_pass) {
+    // two passes (keys, then rows) by default: the fused pass measured 12 %
+    // slower on the theta (n = 20k: 19.7 vs 17.1 s) and 30 % on R-MAT scale
+    // 18 (7.0 vs 5.4 s), 6 % faster on config 4 (155 vs 165 s)
+    static const bool fused = std::getenv("MB_FUSED_HOPS") != nullptr;
+    if (!fused) {
       launch("cycle_hop_keys", [&] { k_hop_expand<0><<<grid_for(W, kHopTile), kHopTile, 0, stream>>>(A); },
              hop_bytes / 2);
       out.n = d2h(nk.as<uint64_t>());
@@ -972,11 +990,12 @@ struct CycleRunner {
     M.out = C.out.data, M.Pout = C.out.P, M.rso = C.out.rs;
     M.scalar = scalar, M.err = err, M.updates = upd;
     M.scalar_mult = h_mult;
+    M.t_mult = h_mult_t;
     if (M.out_kind == 4) {
       ArenaScope no_arena(nullptr);  // the pair table outlives the anchor batch
       // streaming into the root: a full partial table is consumed first
       if (pair_flush && pairs.n && pairs.n * (C.out.P + 2) * 8ull > pair_flush_bytes) pair_flush();
-      reserve_pairs(C.out.P, pairs.n + A.n);
+      reserve_pairs(C.out.P, pairs.n + (h_mult_t ? 2 : 1) * A.n);
       M.ph_key = pairs.key.as<uint64_t>(), M.ph_idx = pairs.idx.as<uint32_t>();
       M.ph_mask = 2 * pairs.cap_rows - 1, M.ph_shift = pairs.shift;
       M.ph_n = reinterpret_cast<unsigned long long*>(pairs.counter.p);
@@ -1144,21 +1163,40 @@ struct CycleRunner {
     }
     static const bool no_sym = std::getenv("MB_NO_CYCLE_SYMMETRY") != nullptr;
     // Eq. 1 positions to evaluate, each with the number of equal terms it stands for
-    std::vector<std::pair<int, uint32_t>> hs;
+    struct HTerm {
+      int h;
+      uint32_t a, b;  // the orbit's Eq. 1 terms: a x T_h + b x (T_h with its pair keys swapped)
+    };
+    std::vector<HTerm> hs;
     if (rotation_symmetric(C) && !no_sym) {
-      hs.push_back({0, static_cast<uint32_t>(C.L)});
+      hs.push_back({0, static_cast<uint32_t>(C.L), 0u});
     } else if (int c2 = reflection_axis(C); c2 >= 0 && !no_sym) {
-      // a reflection p -> c2 - p (mod L) fixes the boundary positions and
+      // a reflection s: p -> c2 - p (mod L) fixes the boundary positions and
       // maps the labelled matches whose highest vertex sits at h one-to-one
-      // onto those with it at the mirrored position, keys and colour sets
-      // unchanged: evaluate one position of each mirrored pair, twice
-      for (int h = 0; h < C.L; ++h) {
-        const int m = ((c2 - h) % C.L + C.L) % C.L;
-        if (m == h) hs.push_back({h, 1u});
-        else if (h < m) hs.push_back({h, 2u});
+      // onto those with it at s(h), keys and colour sets unchanged.  With two
+      // opposite boundary nodes and a pair-keyed output, the rotation r by
+      // L/2 swaps them: T_r(h) is T_h with its keys swapped.  Each orbit of
+      // {1, s, r, rs} is evaluated once (the theta's 6-cycle block: 2 of 6
+      // positions).
+      const int L = C.L;
+      const bool swap_ok = C.bpos.size() == 2 && C.out.kind == 4 && !no_swap_sym();
+      std::vector<char> seen(L, 0);
+      auto refl = [&](int p) { return ((c2 - p) % L + L) % L; };
+      auto rot = [&](int p) { return (p + L / 2) % L; };
+      for (int h = 0; h < L; ++h) {
+        if (seen[h]) continue;
+        const int o1 = refl(h);
+        uint32_t a = 1 + (o1 != h), b = 0;
+        seen[h] = seen[o1] = 1;
+        if (swap_ok) {
+          const int o2 = rot(h), o3 = rot(o1);
+          if (o2 != h && o2 != o1 && !seen[o2]) ++b, seen[o2] = 1;
+          if (o3 != h && o3 != o1 && o3 != o2 && !seen[o3]) ++b, seen[o3] = 1;
+        }
+        hs.push_back({h, a, b});
       }
     } else {
-      for (int h = 0; h < C.L; ++h) hs.push_back({h, 1u});
+      for (int h = 0; h < C.L; ++h) hs.push_back({h, 1u, 0u});
     }
     const int nh = static_cast<int>(hs.size());
     // Anchors are swept in device order (hubs first) with an adaptive batch:
@@ -1185,8 +1223,9 @@ struct CycleRunner {
     };
     static const bool old_batches = std::getenv("MB_HALVING_BATCHES") != nullptr;
     for (int hi = 0; hi < nh; ++hi) {
-      const int h = hs[hi].first;
-      h_mult = hs[hi].second;
+      const int h = hs[hi].h;
+      h_mult = hs[hi].a;
+      h_mult_t = hs[hi].b;
       uint32_t bs = first_batch, cap = first_batch;  // (MB_HALVING_BATCHES) cap: below the last size that failed
       double ratio = 0;  // 0: unknown yet (a first probe batch of 1024 anchors)
       for (uint32_t x0 = 0; x0 < G.n;) {

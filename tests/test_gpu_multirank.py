@@ -28,6 +28,9 @@ QUERIES = {
     "c7": (7, [(i, (i + 1) % 7) for i in range(7)]),
     "c5_pendant": (6, [(0, 1), (1, 2), (2, 3), (3, 4), (4, 0), (2, 5)]),
     "q6": (6, [(0, 1), (1, 2), (2, 0), (1, 3), (3, 2), (2, 4), (4, 5)]),
+    # the pair-producing 6-cycle block is sharded, every rank streams its
+    # partial pair table through the whole root
+    "theta": (8, [(0, 1), (1, 2), (2, 7), (0, 3), (3, 4), (4, 7), (0, 5), (5, 6), (6, 7)]),
 }
 
 
@@ -74,7 +77,7 @@ def test_two_processes_real_engine(mb):
         assert t0 == want and t1 == want, name
         assert [a + b for a, b in zip(p0, p1)] == want, name
         assert d0 == 0 and d1 == 0
-        if name in ("c5", "c7"):  # root cycle blocks with a scalar output are split
+        if name in ("c5", "c7", "theta"):  # root cycle blocks with a scalar output are split
             assert s0 and s1 and all(a > 0 for a in p0) and all(b > 0 for b in p1), name
     rep = mb.estimate(g, mb.QueryPlan(*QUERIES["c5"]), mb.DB, 9, 77)
     for r in (0, 1):
