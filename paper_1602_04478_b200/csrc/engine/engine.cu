@@ -362,6 +362,47 @@ __global__ void k_edge_meta(uint64_t no, const uint32_t* __restrict__ eorder, co
   range[i] = make_ulonglong2(cn_off[j], cn_off[j + 1]);
 }
 
+// Warp-interleaved copy of the CN lists for the lane-per-edge kernels
+// (tri_canon.cuh).  Batch bt holds the 32 edges at eorder positions
+// [32 bt, 32 bt + 32); its lists are cut into 4-entry chunks and chunk ch of
+// lane l is the uint4 at il[(base[bt] + ch) * 32 + l], so one 16-byte load per
+// lane reads 512 contiguous bytes per warp (4 lines instead of 32 lane-private
+// ones).  Lists shorter than the batch's longest are padded with the dummy
+// vertex `pad` (colour 7 in every slot: counted in an unused nibble).
+// k_il_count: nch[bt] = chunks of the batch's longest list.
+__global__ void k_il_count(uint64_t no, const ulonglong2* __restrict__ range, uint64_t* __restrict__ nch) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  uint32_t c = 0;
+  if (i < no) {
+    const ulonglong2 r = range[i];
+    c = static_cast<uint32_t>((r.y - r.x + 3) >> 2);
+  }
+  for (int o = 16; o > 0; o >>= 1) c = max(c, __shfl_xor_sync(0xffffffffu, c, o));
+  if ((threadIdx.x & 31) == 0 && (i >> 5) < ((no + 31) >> 5)) nch[i >> 5] = c;
+}
+__global__ void k_il_fill(uint64_t no, const ulonglong2* __restrict__ range, const uint64_t* __restrict__ nch,
+                          const uint64_t* __restrict__ base, const uint32_t* __restrict__ cw, uint32_t pad,
+                          uint4* __restrict__ il, uint32_t* __restrict__ nch32) {
+  const uint64_t w = (blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x) >> 5;
+  const uint32_t lane = threadIdx.x & 31;
+  if (w >= ((no + 31) >> 5)) return;
+  const uint64_t i = w * 32 + lane;
+  ulonglong2 r = make_ulonglong2(0, 0);
+  if (i < no) r = range[i];
+  const uint32_t n = static_cast<uint32_t>(nch[w]);
+  if (lane == 0) nch32[w] = n;
+  uint4* dst = il + base[w] * 32 + lane;
+  for (uint32_t ch = 0; ch < n; ++ch) {
+    const uint64_t p = r.x + 4ull * ch;
+    uint4 q;
+    q.x = p < r.y ? cw[p] : pad;
+    q.y = p + 1 < r.y ? cw[p + 1] : pad;
+    q.z = p + 2 < r.y ? cw[p + 2] : pad;
+    q.w = p + 3 < r.y ? cw[p + 3] : pad;
+    dst[static_cast<uint64_t>(ch) * 32] = q;
+  }
+}
+
 // Degree-ordered orientation: out(x) = neighbours ranked below x, kept in id
 // order, remembered with their CSR slot.
 __global__ void k_out_degree(uint32_t n, const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,

@@ -212,6 +212,84 @@ __device__ __forceinline__ void lane_histogram_row(const TriHistArgs& A, uint64_
   flushB();
 }
 
+// The same histogram row from the warp-interleaved list copy (TriHistArgs::il):
+// `src` is the lane's first chunk, chunks are 32 uint4 apart, and every lane of
+// the warp runs the batch's `nch` chunks (shorter lists are padded with the
+// dummy vertex A.nv), so the loop is warp-uniform and a warp's chunk load is
+// 512 contiguous bytes.  Chunks are loaded three ahead and their colours
+// gathered one ahead of the counting.
+template <int K>
+__device__ __forceinline__ void lane_histogram_row_il(const TriHistArgs& A, const uint4* __restrict__ src,
+                                                      uint32_t nch, uint16_t* hrow) {
+  uint32_t N[kChiStride], Be[kChiStride], Bo[kChiStride];
+#pragma unroll
+  for (int c = 0; c < kChiStride; ++c) N[c] = Be[c] = Bo[c] = 0;
+  bool spilled = false;
+  auto flushN = [&]() {
+#pragma unroll
+    for (int c = 0; c < kChiStride; ++c) {
+      Be[c] += N[c] & 0x0F0F0F0Fu;
+      Bo[c] += (N[c] >> 4) & 0x0F0F0F0Fu;
+      N[c] = 0;
+    }
+  };
+  auto flushB = [&]() {
+#pragma unroll
+    for (int c = 0; c < kChiStride; ++c) {
+#pragma unroll
+      for (int d = 0; d < K; ++d) {
+        const uint32_t v = (((d & 1) ? Bo[c] : Be[c]) >> (8 * (d >> 1))) & 0xFFu;
+        hrow[c * K + d] = static_cast<uint16_t>(spilled ? hrow[c * K + d] + v : v);
+      }
+      Be[c] = Bo[c] = 0;
+    }
+    spilled = true;
+  };
+  auto gather = [&](const uint4& qq, uint64_t (&cw)[4]) {
+    const uint32_t ws[4] = {qq.x, qq.y, qq.z, qq.w};
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (K < 8) cw[u] = load_colors(A.chi, ws[u]);
+      else cw[u] = ws[u] != A.nv ? load_colors(A.chi, ws[u]) : ~0ull;
+    }
+  };
+  const uint4 pad = make_uint4(A.nv, A.nv, A.nv, A.nv);
+  auto chunk = [&](uint32_t ch) { return ch < nch ? __ldg(src + static_cast<uint64_t>(ch) * 32) : pad; };
+  int pend = 0, nfl = 0;
+  uint4 q1 = chunk(1), q2 = chunk(2);
+  uint64_t cwc[4];
+  gather(chunk(0), cwc);
+  for (uint32_t ch = 0; ch < nch; ++ch) {
+    const uint4 q3 = chunk(ch + 3);
+    uint64_t cwn[4];
+    gather(q1, cwn);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (K == 8 && cwc[u] == ~0ull) continue;
+      const uint32_t lo32 = static_cast<uint32_t>(cwc[u]), hi32 = static_cast<uint32_t>(cwc[u] >> 32);
+#pragma unroll
+      for (int c = 0; c < kChiStride; ++c) {
+        const uint32_t half = c < 4 ? lo32 : hi32;
+        N[c] += nibble_onehot(half, c);
+      }
+    }
+    if (++pend == 3) {
+      flushN();
+      pend = 0;
+      if (++nfl == 20) {
+        flushB();
+        nfl = 0;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) cwc[u] = cwn[u];
+    q1 = q2;
+    q2 = q3;
+  }
+  flushN();
+  flushB();
+}
+
 // K colours; S1 = this block's s_out; FK = pivot factor kind (0 none, 1 node
 // at P0, 2 node at P1, 3 edge (P0, P1)); SP = the fused parent's s_out (0: not
 // fused); NARROW = node factor stored as u32.
@@ -296,7 +374,10 @@ __global__ void __launch_bounds__(32 * kHistWarps, BIL ? MB_BIL_MINB : MB_TRI_MI
     if (jn < A.nitems) emn = A.emeta[jn], ern = A.erange[jn];
     if (jj >= A.nitems) continue;
     const uint32_t a = em.x, b = em.y, sab = em.z, sba = em.w;
-    if (!(A.debug & 2)) lane_histogram_row<K>(A, er.x, er.y, hrow);
+    if (!(A.debug & 2)) {
+      if (A.il) lane_histogram_row_il<K>(A, A.il + __ldg(A.ilbase + bt) * 32 + lane, __ldg(A.ilnch + bt), hrow);
+      else lane_histogram_row<K>(A, er.x, er.y, hrow);
+    }
     if (A.debug & 1) continue;
     const uint64_t cas = load_colors(A.chi, a), cbs = load_colors(A.chi, b);
     uint32_t updl = 0;
@@ -316,7 +397,7 @@ __global__ void __launch_bounds__(32 * kHistWarps, BIL ? MB_BIL_MINB : MB_TRI_MI
           for (int q = 0; q < NB; ++q) Fo[o][q] = 0;
         } else if (FK == 3) {
           const uint64_t s = (o == 0) != (A.sw01 != 0) ? sab : sba;
-          const uint64_t* row = A.F + s * A.rsF + c * A.PF;
+          const uint64_t* row = A.F + s * A.rsF + c * A.psF;
 #pragma unroll
           for (int q = 0; q < NB; ++q) Fo[o][q] = static_cast<FT>(__ldg(row + q));
         } else {
@@ -324,7 +405,7 @@ __global__ void __launch_bounds__(32 * kHistWarps, BIL ? MB_BIL_MINB : MB_TRI_MI
           const uint32_t cf = FK == 1 ? c0 : c1, cx = FK == 1 ? c1 : c0;
           const uint8_t* mp = fmap + (cf * K + cx) * NB;
           const uint32_t pk = PACK ? reinterpret_cast<const uint32_t*>(fmap)[cf * K + cx] : 0u;
-          const uint64_t ro = static_cast<uint64_t>(v) * A.rsF + c * A.PF;
+          const uint64_t ro = static_cast<uint64_t>(v) * A.rsF + c * A.psF;
 #pragma unroll
           for (int q = 0; q < NB; ++q) {
             const uint32_t ix = PACK ? (pk >> (4 * q)) & 15u : mp[q];

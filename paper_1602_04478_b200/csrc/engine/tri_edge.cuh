@@ -306,6 +306,11 @@ struct TriHistArgs {
   const uint32_t* eorder;   // oriented edges in CN-length order (lane_mode)
   const uint4* emeta;       // (a, b, slot a->b, slot b->a) per eorder position
   const ulonglong2* erange; // CN list [lo, hi) per eorder position
+  // warp-interleaved copy of the lists (k_il_fill): chunk ch of lane l of batch
+  // bt is il[(ilbase[bt] + ch) * 32 + l]; ilnch[bt] chunks per lane
+  const uint4* il;
+  const uint64_t* ilbase;
+  const uint32_t* ilnch;
   // stage 1: this block
   int s_out;
   uint32_t P2;          // C(k-2, s_out-2): entries of S containing both pivot colours
@@ -313,6 +318,7 @@ struct TriHistArgs {
   int fkind;            // pivot factor: 0 none, 1 node at P0, 2 node at P1, 3 edge (P0,P1)
   const uint64_t* F;    // table base (colouring 0)
   uint32_t PF, rsF;
+  uint32_t psF;         // per-colouring row stride of F (PF, or PF rounded up to 4 for 16-byte rows)
   int sw01;             // edge factor stored keyed (P1, P0)
   int out_kind;         // 0 scalar, 1 unary keyed by img P0, 2 edge keyed (img P0, img P1), 3 fused
   uint64_t* out;
@@ -536,9 +542,9 @@ __global__ void __launch_bounds__(32 * kHistWarps, MB_TRI_MINB) tri_hist_kernel(
             // stage this orientation's factor row: independent loads in
             // flight together instead of one dependent gather per term
             uint64_t fo;
-            if (A.fkind == 1) fo = static_cast<uint64_t>(o ? b : a) * A.rsF + c * A.PF;
-            else if (A.fkind == 2) fo = static_cast<uint64_t>(o ? a : b) * A.rsF + c * A.PF;
-            else fo = static_cast<uint64_t>((o == 0) != (A.sw01 != 0) ? sab : sba) * A.rsF + c * A.PF;
+            if (A.fkind == 1) fo = static_cast<uint64_t>(o ? b : a) * A.rsF + c * A.psF;
+            else if (A.fkind == 2) fo = static_cast<uint64_t>(o ? a : b) * A.rsF + c * A.psF;
+            else fo = static_cast<uint64_t>((o == 0) != (A.sw01 != 0) ? sab : sba) * A.rsF + c * A.psF;
             const uint64_t* F = A.F + fo;
             const uint32_t* F32 = reinterpret_cast<const uint32_t*>(A.F) + fo;
             if (NARROW) {
