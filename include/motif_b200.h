@@ -104,6 +104,23 @@ int mb_count_colorful_seeds(mb_graph* g, mb_plan* p, const uint64_t* seeds, int 
  * the root block was split, 0 when rank 0 returned the whole count. */
 int mb_count_colorful_shard(mb_graph* g, mb_plan* p, const uint8_t* chi, int ncol, int engine,
                             int rank, int world, uint64_t* partial, int* split);
+/* Vertex-sharded count with table exchange: as
+ * mb_count_colorful_shard, and in addition every leaf block of the plan is
+ * computed for this rank's vertices only and its rows are exchanged — the
+ * reference's BSP rounds ship table entries to the owner of their key vertex
+ * (redistribute / extend, runtime.cpp:94-114, 173-202); here each rank packs
+ * its rows into slice `rank` of a DEVICE buffer of `world` slices of
+ * `bytes_per_rank` bytes and calls `allgather(ctx, buf, bytes_per_rank)`, which
+ * must fill the other slices with the other ranks' (an in-place all-gather:
+ * ncclAllGather on the caller's communicator, or a host-staged gather) and
+ * return 0 once the data is in place.  Every rank makes the same sequence of
+ * calls.  A root 3-cycle block with a scalar output is dealt over the ranks
+ * by warp batch of oriented edges, a root cycle block by anchor vertex, a
+ * root leaf block by vertex; *split as above. */
+typedef int (*mb_allgather_fn)(void* ctx, void* dev_buf, uint64_t bytes_per_rank);
+int mb_count_colorful_sharded(mb_graph* g, mb_plan* p, const uint8_t* chi, int ncol, int engine,
+                              int rank, int world, mb_allgather_fn allgather, void* ctx,
+                              uint64_t* partial, int* split);
 /* Device-resident colourings (n*ncol bytes, colours 1..k, cudaMalloc'd). */
 int mb_count_colorful_device(mb_graph* g, mb_plan* p, const uint8_t* chi_dev, int ncol,
                              uint64_t* out);
@@ -151,6 +168,8 @@ int mb_engine_device(const mb_graph* g);
 /* Milliseconds spent building plan-derived graph indexes (triangle lists). */
 double mb_engine_prep_ms(mb_graph* g);
 uint64_t mb_engine_launches(mb_graph* g);
+/* Bytes this rank has received through mb_count_colorful_sharded's exchanges. */
+uint64_t mb_engine_exchanged_bytes(mb_graph* g);
 int mb_engine_stats(mb_graph* g, uint64_t* triangles, uint64_t* table_bytes,
                     uint64_t* dp_updates);
 /* Drop plan-derived graph structures so the next count rebuilds them. */

@@ -42,7 +42,7 @@ __all__ = [
     "MotifError", "ParseError", "TreewidthError", "CountOverflowError", "BudgetError",
     "SchemaError", "ContractError", "SpecError", "CudaError",
     "DataGraph", "QueryPlan", "EstimateReport", "Partition", "load_edge_list", "degree_rank",
-    "random_coloring", "derive_seed", "count_colorful", "count_colorful_shard", "estimate", "automorphism_count",
+    "random_coloring", "derive_seed", "count_colorful", "count_colorful_shard", "count_colorful_sharded", "estimate", "automorphism_count",
     "normalization_factor", "coefficient_of_variation", "estimate_from_counts", "PS", "DB", "lib",
 ]
 
@@ -89,6 +89,10 @@ _ERRORS = {c.code: c for c in (ParseError, TreewidthError, CountOverflowError, B
                                 SchemaError, ContractError, SpecError, CudaError)}
 
 
+# mb_allgather_fn (include/motif_b200.h): int (*)(void* ctx, void* dev_buf, uint64_t bytes_per_rank)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64)
+
+
 def _load() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -131,6 +135,8 @@ def _load() -> C.CDLL:
         "mb_count_colorful_device": (C.c_int, [P, P, C.c_void_p, C.c_int, u64p]),
         "mb_count_colorful_shard": (C.c_int, [P, P, u8p, C.c_int, C.c_int, C.c_int, C.c_int, u64p,
                                               C.POINTER(C.c_int)]),
+        "mb_count_colorful_sharded": (C.c_int, [P, P, u8p, C.c_int, C.c_int, C.c_int, C.c_int, ALLGATHER_FN,
+                                                C.c_void_p, u64p, C.POINTER(C.c_int)]),
         "mb_automorphism_count": (C.c_int, [C.c_int, i32p, C.c_int, u64p]),
         "mb_normalization_factor": (C.c_double, [C.c_int]),
         "mb_coefficient_of_variation": (C.c_double, [u64p, C.c_uint64]),
@@ -147,6 +153,7 @@ def _load() -> C.CDLL:
         "mb_engine_device": (C.c_int, [P]),
         "mb_engine_prep_ms": (C.c_double, [P]),
         "mb_engine_launches": (C.c_uint64, [P]),
+        "mb_engine_exchanged_bytes": (C.c_uint64, [P]),
         "mb_engine_stats": (C.c_int, [P, u64p, u64p, u64p]),
         "mb_engine_reset_derived": (C.c_int, [P]),
         "mb_engine_release": (C.c_int, [P]),
@@ -366,6 +373,38 @@ def count_colorful_shard(g: DataGraph, plan: QueryPlan, chi: np.ndarray, rank: i
     return out, bool(split.value)
 
 
+def count_colorful_sharded(g: DataGraph, plan: QueryPlan, chi: np.ndarray, rank: int, world: int, allgather,
+                           engine: int = DB) -> tuple[np.ndarray, bool]:
+    """mb_count_colorful_sharded: this rank's partial counts with the leaf
+    blocks computed for its own vertices and their rows exchanged through
+    ``allgather(dev_ptr, bytes_per_rank)`` (an in-place all-gather over a
+    device buffer of ``world`` slices; see parallel.make_allgather)."""
+    a = np.ascontiguousarray(np.atleast_2d(chi), dtype=np.uint8)
+    if a.shape[1] != g.num_vertices():
+        raise SpecError("colouring length != number of vertices")
+    out = np.zeros(a.shape[0], dtype=np.uint64)
+    split = C.c_int()
+    failure: list[BaseException] = []
+
+    def _cb(_ctx, ptr, nbytes):
+        try:
+            allgather(int(ptr), int(nbytes))
+            return 0
+        except BaseException as e:  # surfaces as CudaError below, with the cause attached
+            failure.append(e)
+            return 1
+
+    cb = ALLGATHER_FN(_cb)
+    try:
+        _check(lib.mb_count_colorful_sharded(g.handle, plan.handle, _ptr(a, C.c_uint8), a.shape[0], engine, rank,
+                                             world, cb, None, _ptr(out, C.c_uint64), C.byref(split)))
+    except MotifError as e:
+        if failure:
+            raise e from failure[0]
+        raise
+    return out, bool(split.value)
+
+
 def count_colorful_device(g: DataGraph, plan: QueryPlan, chi_dev_ptr: int, ncol: int) -> np.ndarray:
     out = np.zeros(ncol, dtype=np.uint64)
     _check(lib.mb_count_colorful_device(g.handle, plan.handle, C.c_void_p(chi_dev_ptr), ncol,
@@ -483,6 +522,11 @@ def engine_stream(g: DataGraph) -> int:
 
 def engine_launches(g: DataGraph) -> int:
     return lib.mb_engine_launches(g.handle)
+
+
+def engine_exchanged_bytes(g: DataGraph) -> int:
+    """Bytes this rank received through count_colorful_sharded's exchanges."""
+    return lib.mb_engine_exchanged_bytes(g.handle)
 
 
 def engine_prep_ms(g: DataGraph) -> float:

@@ -275,6 +275,33 @@ int mb_count_colorful_shard(mb_graph* g, mb_plan* p, const uint8_t* chi, int nco
   });
 }
 
+int mb_count_colorful_sharded(mb_graph* g, mb_plan* p, const uint8_t* chi, int ncol, int engine, int rank, int world,
+                              mb_allgather_fn allgather, void* ctx, uint64_t* partial, int* split) {
+  return guarded([&] {
+    if (engine != 0 && engine != 1) mb::fail(mb::kSpec, "engine must be 0 (PS) or 1 (DB)");
+    if (world < 1 || rank < 0 || rank >= world) mb::fail(mb::kSpec, "shard rank out of range");
+    if (!allgather && world > 1) mb::fail(mb::kSpec, "sharded count needs an all-gather callback");
+    auto& eng = engine_for(g, p);
+    eng.set_shard(static_cast<uint32_t>(rank), static_cast<uint32_t>(world));
+    if (world > 1)
+      eng.set_exchange([allgather, ctx](void* buf, uint64_t bytes) {
+        if (allgather(ctx, buf, bytes) != 0) mb::fail(mb::kCuda, "table exchange (all-gather callback) failed");
+      });
+    auto reset = [&] {
+      eng.set_exchange(nullptr);
+      eng.set_shard(0, 1);
+    };
+    try {
+      if (split) *split = eng.root_shardable() ? 1 : 0;
+      eng.count(chi, ncol, true, partial);
+    } catch (...) {
+      reset();
+      throw;
+    }
+    reset();
+  });
+}
+
 int mb_count_colorful_device(mb_graph* g, mb_plan* p, const uint8_t* chi_dev, int ncol, uint64_t* out) {
   return guarded([&] { engine_for(g, p).count(chi_dev, ncol, false, out); });
 }
@@ -391,6 +418,7 @@ int mb_engine_device(const mb_graph* g) { return g->eng ? g->eng->device() : -1;
 double mb_engine_prep_ms(mb_graph* g) { return g->eng ? g->eng->stats().prep_ms : 0.0; }
 
 uint64_t mb_engine_launches(mb_graph* g) { return g->eng ? g->eng->launches() : 0; }
+uint64_t mb_engine_exchanged_bytes(mb_graph* g) { return g->eng ? g->eng->exchanged_bytes() : 0; }
 
 int mb_engine_stats(mb_graph* g, uint64_t* triangles, uint64_t* table_bytes, uint64_t* dp_updates) {
   return guarded([&] {

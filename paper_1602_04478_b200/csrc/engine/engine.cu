@@ -403,6 +403,33 @@ __global__ void k_il_fill(uint64_t no, const ulonglong2* __restrict__ range, con
   }
 }
 
+// Table exchange of vertex-sharded leaf blocks (GpuEngine::set_exchange): rank
+// r owns the device vertices v with v % world == r; its rows are packed in
+// ownership order (row i of the slice = vertex i * world + r) into slice r of
+// the exchange buffer, and the other ranks' slices are scattered back into the
+// table after the all-gather.  Rows are copied in units of U bytes.
+template <class U>
+__global__ void k_rows_pack(const U* __restrict__ table, U* __restrict__ slice, uint32_t n, uint32_t rank,
+                            uint32_t world, uint64_t units_per_row, uint64_t rows) {
+  const uint64_t idx = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (idx >= rows * units_per_row) return;
+  const uint64_t i = idx / units_per_row, u = idx - i * units_per_row;
+  const uint64_t v = i * world + rank;
+  if (v < n) slice[idx] = table[v * units_per_row + u];
+}
+template <class U>
+__global__ void k_rows_unpack(U* __restrict__ table, const U* __restrict__ buf, uint32_t n, uint32_t rank,
+                              uint32_t world, uint64_t units_per_row, uint64_t rows) {
+  const uint64_t idx = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const uint64_t per = rows * units_per_row;
+  if (idx >= per * world) return;
+  const uint64_t q = idx / per, r = idx - q * per;
+  if (q == rank) return;
+  const uint64_t i = r / units_per_row, u = r - i * units_per_row;
+  const uint64_t v = i * world + q;
+  if (v < n) table[v * units_per_row + u] = buf[idx];
+}
+
 // Degree-ordered orientation: out(x) = neighbours ranked below x, kept in id
 // order, remembered with their CSR slot.
 __global__ void k_out_degree(uint32_t n, const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,

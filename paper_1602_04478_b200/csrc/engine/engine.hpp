@@ -16,6 +16,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -78,6 +79,18 @@ class GpuEngine {
   // otherwise rank 0 returns the whole count and the other ranks 0.
   void set_shard(uint32_t rank, uint32_t world);
   bool root_shardable() const;
+  // Table exchange for sharded leaf blocks (the reference's
+  // redistribute / extend shipping rows to their owners, runtime.cpp:94-114,
+  // 173-202): with an exchange set, every leaf block computes only the rows of
+  // this rank's vertices, packs them into slice `rank` of a device buffer of
+  // `world` equal slices and calls the exchange, which must fill the other
+  // slices with the other ranks' rows (an in-place all-gather: NCCL on
+  // NVLink, or staged through the host); the rows are then unpacked so every
+  // rank holds the whole table again.  Blocks above the leaves read whole
+  // tables, so only these rows ever cross ranks.
+  using AllGather = std::function<void(void* dev_buf, uint64_t bytes_per_rank)>;
+  void set_exchange(AllGather fn);
+  uint64_t exchanged_bytes() const;  // bytes received through the exchange so far
 
   struct Impl;
 

@@ -361,8 +361,11 @@ __global__ void __launch_bounds__(32 * kHistWarps, BIL ? MB_BIL_MINB : MB_TRI_MI
   const uint64_t nbatch = (A.nitems + 31) / 32;
   // edge metadata one iteration ahead (its DRAM latency would otherwise
   // stall every edge)
-  const uint64_t bstride = static_cast<uint64_t>(gridDim.x) * kHistWarps;
-  uint64_t bt = static_cast<uint64_t>(blockIdx.x) * kHistWarps + wid;
+  // vertex sharding (TriHistArgs::shard_*): this rank visits the warp batches
+  // bt with bt % world == rank (list-length order: every rank gets its share
+  // of long and short lists)
+  const uint64_t bstride = static_cast<uint64_t>(gridDim.x) * kHistWarps * A.shard_world;
+  uint64_t bt = (static_cast<uint64_t>(blockIdx.x) * kHistWarps + wid) * A.shard_world + A.shard_rank;
   uint4 emn = make_uint4(0, 0, 0, 0);
   ulonglong2 ern = make_ulonglong2(0, 0);
   if (bt * 32 + lane < A.nitems) emn = A.emeta[bt * 32 + lane], ern = A.erange[bt * 32 + lane];

@@ -311,6 +311,7 @@ struct TriHistArgs {
   const uint4* il;
   const uint64_t* ilbase;
   const uint32_t* ilnch;
+  uint32_t shard_rank, shard_world;  // tri_canon_kernel: warp batches dealt over ranks (1 = all)
   // stage 1: this block
   int s_out;
   uint32_t P2;          // C(k-2, s_out-2): entries of S containing both pivot colours

@@ -17,6 +17,15 @@ Two shardings, both without a data-path collective:
   are added with one all-reduce (the reference's sharded total,
   runtime.cpp:297-302).  See DESIGN.md §6.
 
+  With ``exchange=True`` the leaf blocks are sharded as well: every rank
+  computes the rows of its own vertices and the rows are exchanged with an
+  all-gather per leaf table (``make_allgather``: NCCL in place on the device
+  buffer, or staged through the host for gloo) — the halo exchange the
+  reference performs when redistribute / extend ship entries to the owner of
+  their key vertex (runtime.cpp:94-114, 173-202) — and a root 3-cycle block
+  is dealt over the ranks by warp batch of oriented edges
+  (mb_count_colorful_sharded).
+
 Results are bit-identical to the single-GPU call for every world size.
 ``count_fn`` lets the CPU tests drive the same plumbing with the oracle.
 """
@@ -112,8 +121,56 @@ def sum_partials(parts: Sequence[Sequence[int]], overflowed: Sequence[bool]) -> 
     return np.asarray(tot, dtype=np.uint64)
 
 
+class _DeviceBytes:
+    """A raw device allocation as a __cuda_array_interface__ object, so that
+    torch can wrap the engine's exchange buffer without copying it."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 2}
+
+
+def gather_slices(slices: Sequence[np.ndarray]) -> np.ndarray:
+    """The exchange buffer after the all-gather: rank q's packed rows in slice
+    q (host-side model of the layout, used by the CPU tests)."""
+    return np.concatenate([np.asarray(s, dtype=np.uint8) for s in slices])
+
+
+def make_allgather(dist, world: int, rank: int, device=None):
+    """The ``allgather(dev_ptr, bytes_per_rank)`` callback of
+    count_colorful_sharded over torch.distributed: the engine has packed this
+    rank's rows into slice ``rank`` of the device buffer; on return every slice
+    holds its rank's rows.  NCCL gathers in place on the device (NVLink);
+    other backends stage the slices through host memory."""
+    import torch
+
+    nccl = dist.get_backend() == "nccl"
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+
+    on_host = torch.device(device).type == "cpu"  # CPU tests: the buffer is host memory
+
+    def allgather(ptr: int, nbytes: int) -> None:
+        if on_host:
+            import ctypes
+
+            buf = torch.from_numpy(np.ctypeslib.as_array((ctypes.c_uint8 * (nbytes * world)).from_address(ptr)))
+        else:
+            buf = torch.as_tensor(_DeviceBytes(ptr, nbytes * world), device=device)
+        mine = buf[rank * nbytes:(rank + 1) * nbytes]
+        if nccl:
+            dist.all_gather_into_tensor(buf, mine.clone())
+        else:
+            parts = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(world)]
+            dist.all_gather(parts, mine.cpu())
+            buf.copy_(torch.from_numpy(gather_slices([p.numpy() for p in parts])))
+        if not on_host:
+            torch.cuda.synchronize(device)
+
+    return allgather
+
+
 def distributed_count_vertex_sharded(g, plan, chis, engine: int = 1, count_fn: Callable | None = None,
-                                     device=None) -> np.ndarray:
+                                     device=None, exchange: bool = False) -> np.ndarray:
     """Counts of the colourings `chis` (c, n) with the data-graph vertices
     sharded over the ranks: each rank sums the root-block matches anchored at
     its vertices (mb_count_colorful_shard), and the partials are combined by
@@ -123,7 +180,7 @@ def distributed_count_vertex_sharded(g, plan, chis, engine: int = 1, count_fn: C
     call in the CPU tests."""
     import torch
 
-    from . import CountOverflowError, count_colorful_shard
+    from . import CountOverflowError, count_colorful_shard, count_colorful_sharded
 
     dist, world, rank = _world()
     chis = np.atleast_2d(chis)
@@ -133,7 +190,10 @@ def distributed_count_vertex_sharded(g, plan, chis, engine: int = 1, count_fn: C
         part = np.asarray(part, dtype=np.uint64)
     else:
         try:
-            part, _ = count_colorful_shard(g, plan, chis, rank, world, engine)
+            if exchange and world > 1:
+                part, _ = count_colorful_sharded(g, plan, chis, rank, world, make_allgather(dist, world, rank), engine)
+            else:
+                part, _ = count_colorful_shard(g, plan, chis, rank, world, engine)
         except CountOverflowError:
             part, overflowed = np.zeros(len(chis), np.uint64), True
     if world == 1:

@@ -31,6 +31,12 @@ QUERIES = {
     # the pair-producing 6-cycle block is sharded, every rank streams its
     # partial pair table through the whole root
     "theta": (8, [(0, 1), (1, 2), (2, 7), (0, 3), (3, 4), (4, 7), (0, 5), (5, 6), (6, 7)]),
+    # leaf blocks only: with the table exchange every level is sharded and the
+    # root leaf's rows are totalled per rank
+    "path5": (5, [(0, 1), (1, 2), (2, 3), (3, 4)]),
+    "star_path": (6, [(0, 1), (0, 2), (0, 3), (3, 4), (4, 5)]),
+    # triangle with pendant trees: leaf tables feed a 3-cycle root
+    "tri_tails": (6, [(0, 1), (1, 2), (2, 0), (0, 3), (1, 4), (4, 5)]),
 }
 
 
@@ -54,7 +60,14 @@ def _worker(rank, world, port, results):
             chis = np.stack([mb.random_coloring(g, k, s) for s in (3, 4, 5)])
             part, split = mb.count_colorful_shard(g, plan, chis, rank, world)
             tot = parallel.distributed_count_vertex_sharded(g, plan, chis, device="cpu")
-            out[name] = ([int(x) for x in part], split, [int(x) for x in tot], mb.engine_device(g))
+            # the same with the leaf blocks sharded and their rows exchanged
+            # (gloo: staged through the host; both ranks share cuda:0)
+            ag = parallel.make_allgather(dist, world, rank)
+            xpart, xsplit = mb.count_colorful_sharded(g, plan, chis, rank, world, ag)
+            xtot = parallel.distributed_count_vertex_sharded(g, plan, chis, device="cpu", exchange=True)
+            out[name] = ([int(x) for x in part], split, [int(x) for x in tot], mb.engine_device(g),
+                         [int(x) for x in xpart], xsplit, [int(x) for x in xtot])
+            out[name + "/bytes"] = mb.engine_exchanged_bytes(g)
         plan = mb.QueryPlan(*QUERIES["c5"])
         rep = parallel.distributed_estimate(g, plan, mb.DB, 9, 77, device="cpu")
         out["estimate"] = (rep.per_trial_colorful, rep.mean_estimate, rep.cv)
@@ -63,23 +76,41 @@ def _worker(rank, world, port, results):
         dist.destroy_process_group()
 
 
-def test_two_processes_real_engine(mb):
+@pytest.mark.parametrize("world", [2, 3])
+def test_processes_real_engine(mb, world):
     mgr = mp.Manager()
     results = mgr.dict()
-    mp.spawn(_worker, args=(2, _free_port(), results), nprocs=2, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), results), nprocs=world, join=True)
     g = mb.DataGraph.chung_lu(3000, 2.1, 8.0, 11)
     for name, (k, q) in QUERIES.items():
         plan = mb.QueryPlan(k, q)
         chis = np.stack([mb.random_coloring(g, k, s) for s in (3, 4, 5)])
         want = [int(x) for x in mb.count_colorful(g, plan, chis)]
-        p0, s0, t0, d0 = results[0][name]
-        p1, s1, t1, d1 = results[1][name]
-        assert t0 == want and t1 == want, name
-        assert [a + b for a, b in zip(p0, p1)] == want, name
-        assert d0 == 0 and d1 == 0
-        if name in ("c5", "c7", "theta"):  # root cycle blocks with a scalar output are split
-            assert s0 and s1 and all(a > 0 for a in p0) and all(b > 0 for b in p1), name
+        rows = [results[r][name] for r in range(world)]
+        parts, splits = [r[0] for r in rows], [r[1] for r in rows]
+        assert all(r[2] == want for r in rows), name
+        assert [sum(col) for col in zip(*parts)] == want, name
+        assert all(r[3] == 0 for r in rows)
+        # root cycle blocks with a scalar output are split by anchor, root
+        # 3-cycle blocks on the relative-colour kernel by warp batch
+        if name in ("c5", "c7", "theta", "q6"):
+            assert all(splits) and all(x > 0 for p in parts for x in p), name
+        # with the table exchange: same totals, and leaf roots are split too
+        xparts, xsplits = [r[4] for r in rows], [r[5] for r in rows]
+        assert all(r[6] == want for r in rows), name
+        assert [sum(col) for col in zip(*xparts)] == want, name
+        assert len(set(xsplits)) == 1, name
+        if name in ("c5", "c7", "theta", "q6", "path5", "star_path"):
+            assert xsplits[0] and all(x > 0 for p in xparts for x in p), name
+    # plans with leaf blocks below the root moved rows between the ranks
+    for r in range(world):
+        seen = 0
+        for name in QUERIES:
+            now = results[r][name + "/bytes"]
+            if name in ("c5_pendant", "q6", "path5", "star_path", "tri_tails"):
+                assert now > seen, name
+            seen = now
     rep = mb.estimate(g, mb.QueryPlan(*QUERIES["c5"]), mb.DB, 9, 77)
-    for r in (0, 1):
+    for r in range(world):
         per, mean, cv = results[r]["estimate"]
         assert per == rep.per_trial_colorful and mean == rep.mean_estimate and cv == rep.cv

@@ -125,7 +125,16 @@ def _shard_worker(rank, world, port, results):
             over1 = "none"
         except CountOverflowError:
             over1 = "rank"
-        results[rank] = ([int(x) for x in got], want, over, over1)
+        # the table-exchange callback (parallel.make_allgather) on host memory:
+        # this rank's packed rows sit in slice `rank`; afterwards every slice
+        # holds its rank's rows
+        nbytes = 4096 + 16
+        xbuf = np.zeros(world * nbytes, np.uint8)
+        xbuf[rank * nbytes:(rank + 1) * nbytes] = (np.arange(nbytes) * (rank + 3) + rank) % 251
+        parallel.make_allgather(dist, world, rank, device="cpu")(xbuf.ctypes.data, nbytes)
+        xok = all(np.array_equal(xbuf[q * nbytes:(q + 1) * nbytes], (np.arange(nbytes) * (q + 3) + q) % 251)
+                  for q in range(world))
+        results[rank] = ([int(x) for x in got], want, over, over1, xok)
     finally:
         dist.destroy_process_group()
 
@@ -138,6 +147,7 @@ def test_two_ranks_gloo_vertex_sharded_sum():
     results = mgr.dict()
     mp.spawn(_shard_worker, args=(2, _free_port(), results), nprocs=2, join=True)
     for rank in (0, 1):
-        got, want, over, over1 = results[rank]
+        got, want, over, over1, xok = results[rank]
         assert got == want
         assert over == "sum" and over1 == "rank"
+        assert xok
