@@ -65,6 +65,14 @@ struct HopArgs {
   const uint64_t* woff;  // exclusive scan of per-entry work (n_in + 1)
   const uint64_t* sstart;  // per entry: first relation slot walked
   uint64_t W;
+  const uint64_t* tstart;  // per tile of kHopTile items: the entry of its first item (k_tile_starts)
+  // per-item results of the keys pass, read back by the accumulate pass: the
+  // hash slot of the item's output key (~0u: the item was dropped) and the
+  // colour of its new vertex
+  uint32_t* item_slot;     // (k_slot_to_index turns the slots into dense row indices between the passes)
+  uint16_t* item_col;      // colours of the item's (x, v, w), 4 bits each
+  const uint8_t* ecol;     // per frontier entry: colours of (x, v), 4 bits each (k_hop_work)
+  int unchecked;           // host bound: no output entry can reach 2^63 (plain adds, no return value)
   // hop relation: rows roff/radj (graph CSR or a pair table's CSR)
   const uint64_t* roff;
   const uint32_t* radj;
@@ -102,21 +110,22 @@ __device__ __forceinline__ uint64_t ht_slot(uint64_t key, int shift) {
 }
 
 // Inserts `key` (keys pass): the first inserter takes the next dense index.
-__device__ __forceinline__ void ht_insert(uint64_t* ht_key, uint32_t* ht_idx, uint64_t mask, int shift, uint64_t key,
-                                          unsigned long long* n_keys, uint64_t* key_out) {
+// Returns the key's slot.
+__device__ __forceinline__ uint64_t ht_insert(uint64_t* ht_key, uint32_t* ht_idx, uint64_t mask, int shift,
+                                              uint64_t key, unsigned long long* n_keys, uint64_t* key_out) {
   uint64_t h = ht_slot(key, shift);
   while (true) {
     const uint64_t cur = ht_key[h];
-    if (cur == key) return;
+    if (cur == key) return h;
     if (cur == kEmptyKey) {
       const uint64_t prev = atomicCAS(reinterpret_cast<unsigned long long*>(ht_key + h), kEmptyKey, key);
       if (prev == kEmptyKey) {
         const uint32_t idx = static_cast<uint32_t>(atomicAdd(n_keys, 1ull));
         ht_idx[h] = idx;
         key_out[idx] = key;
-        return;
+        return h;
       }
-      if (prev == key) return;
+      if (prev == key) return h;
     }
     h = (h + 1) & mask;
   }
@@ -191,11 +200,16 @@ __device__ __forceinline__ void unpack_key(uint64_t key, int has_r, int bits, ui
 // neighbours that would only be discarded.
 __global__ void k_hop_work(const uint64_t* __restrict__ key_in, uint64_t n_in, int has_r, int bits,
                            const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj, int ordered,
-                           uint64_t* __restrict__ work, uint64_t* __restrict__ sstart) {
+                           uint64_t* __restrict__ work, uint64_t* __restrict__ sstart,
+                           const uint8_t* __restrict__ chi, uint32_t n, uint8_t* __restrict__ ecol) {
   const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
   if (i >= n_in) return;
   uint32_t x, v, r;
   unpack_key(key_in[i], has_r, bits, x, v, r);
+  // the entry's key colours, read once here instead of once per work item
+  ecol[i] = (x < n && v < n) ? static_cast<uint8_t>(chi[static_cast<uint64_t>(x) * kChiStride] |
+                                                   (chi[static_cast<uint64_t>(v) * kChiStride] << 4))
+                             : 0;
   uint64_t lo = off[v], hi = off[v + 1];
   if (ordered) {
     uint64_t a = lo, b = hi;  // first slot with adj > x
@@ -231,6 +245,34 @@ __global__ void k_suffix_work(uint32_t n, const uint64_t* __restrict__ off, cons
 
 constexpr int kHopTile = 256;  // items per CTA of k_hop_expand
 
+// tstart[t] = the frontier entry holding item t * kHopTile (the last i with
+// woff[i] <= item), tstart[ntiles] = the entry of the last item: a thread per
+// tile, so the binary searches of a hop run in parallel instead of one per
+// CTA of k_hop_expand in front of a barrier (ncu: 25 % of that kernel's stall
+// samples sat on the barrier).
+__global__ void k_tile_starts(const uint64_t* __restrict__ woff, uint64_t n_in, uint64_t W, uint64_t ntiles,
+                              uint64_t* __restrict__ tstart) {
+  const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (t > ntiles) return;
+  const uint64_t it = min(t * kHopTile, W - 1);
+  uint64_t lo = 0, hi = n_in;
+  while (hi - lo > 1) {
+    const uint64_t mid = (lo + hi) >> 1;
+    if (woff[mid] <= it) lo = mid; else hi = mid;
+  }
+  tstart[t] = lo;
+}
+
+// Between the passes: every live item's hash slot becomes the dense row index
+// its key was given (one independent gather per thread, instead of a probe at
+// the head of each accumulate thread's dependent chain).
+__global__ void k_slot_to_index(uint32_t* __restrict__ item_slot, const uint32_t* __restrict__ ht_idx, uint64_t W) {
+  const uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (i >= W) return;
+  const uint32_t s = item_slot[i];
+  if (s != ~0u) item_slot[i] = ht_idx[s];
+}
+
 // One thread per (frontier entry, neighbour) work item, two passes over the
 // same items.  KEYS: the item's output key (x, w[, r]) is inserted into an
 // open-addressing hash table that hands out dense indices.  ACCUMULATE: the
@@ -245,7 +287,6 @@ template <int MODE>
 __global__ void __launch_bounds__(kHopTile) k_hop_expand(HopArgs A) {
   constexpr bool KEYS = MODE == 0;
   __shared__ uint64_t s_woff[kHopTile + 1];
-  __shared__ uint64_t s_e0, s_cnt;
   __shared__ uint32_t s_binom[KEYS ? 1 : (kMaxColors + 1) * kBinomStride];
   if (!KEYS) stage_binom(c_lut, s_binom);
   const uint64_t item0 = static_cast<uint64_t>(blockIdx.x) * kHopTile;
@@ -258,14 +299,8 @@ __global__ void __launch_bounds__(kHopTile) k_hop_expand(HopArgs A) {
     }
     return lo;
   };
-  if (threadIdx.x == 0) {
-    const uint64_t e0 = entry_of(item0);
-    const uint64_t e1 = entry_of(min(item0 + kHopTile - 1, A.W - 1));
-    s_e0 = e0;
-    s_cnt = e1 - e0 + 1;
-  }
-  __syncthreads();
-  const uint64_t e0 = s_e0, cnt = s_cnt;
+  // the tile's entries lie in [tstart[b], tstart[b + 1]] (k_tile_starts)
+  const uint64_t e0 = A.tstart[blockIdx.x], cnt = A.tstart[blockIdx.x + 1] - e0 + 1;
   const bool staged = cnt <= kHopTile;
   if (staged)
     for (uint64_t j = threadIdx.x; j <= cnt && e0 + j <= A.n_in; j += kHopTile) s_woff[j] = A.woff[e0 + j];
@@ -282,8 +317,50 @@ __global__ void __launch_bounds__(kHopTile) k_hop_expand(HopArgs A) {
   } else {
     i = entry_of(item);
   }
+  // Plain hops (no edge or node table joined at the new vertex): the keys
+  // pass left each live item's row index (via k_slot_to_index) and colours, so
+  // the accumulate pass reads neither the key, the neighbour nor the hash
+  // table again; the input row is loaded four entries at a time (independent
+  // loads) and, under the host's bound, added with plain reductions.
+  if (MODE == 1 && !A.etab && !A.ntab) {
+    const uint32_t oi = A.item_slot[item];
+    if (oi == ~0u) return;
+    const uint32_t col = A.item_col[item];
+    const uint32_t cx = col & 15u, cv = (col >> 4) & 15u, cw = col >> 8;
+    const uint32_t fin = A.first_hop ? (1u << cx) : ((1u << cx) | (1u << cv));
+    const uint32_t fw = 1u << cw, fout = (1u << cx) | fw;
+    u64* row = reinterpret_cast<u64*>(A.row_out + static_cast<uint64_t>(oi) * A.P_out);
+    const uint64_t* prow = A.pay_in + i * A.P_in;
+    const int t_in = A.s_in - mb_popc(fin);
+    uint32_t nupd = 0;
+    for (uint32_t b = 0; b < A.P_in; b += 4) {
+      uint64_t pv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) pv[u] = b + u < A.P_in ? prow[b + u] : 0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (!pv[u]) continue;
+        const uint32_t Sin = sig_expand(sig_unrank(c_lut, t_in, b + u), fin);
+        if (Sin & fw) continue;
+        const uint32_t S2 = Sin | fw;
+        const uint32_t o = sig_index_sm(s_binom, S2, fout);
+        if (o >= A.P_out || mb_popc(S2) != A.s_out) {
+          atomicOr(A.err, 16);
+          continue;
+        }
+        if (A.unchecked) atomicAdd(row + o, static_cast<u64>(pv[u]));
+        else atomic_add_ck(row + o, pv[u], A.err);
+        ++nupd;
+      }
+    }
+    const unsigned am = __activemask();
+    const unsigned tot = __reduce_add_sync(am, nupd);
+    if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(am) - 1) && tot) atomicAdd(A.updates, static_cast<u64>(tot));
+    return;
+  }
   uint32_t x, v, r;
   unpack_key(A.key_in[i], A.in_has_r, A.bits, x, v, r);
+  if (MODE == 0) A.item_slot[item] = ~0u;  // until the item proves live below
   if (x >= A.G.n || v >= A.G.n) {
     if (MODE != 1) atomicOr(A.err, 32);
     return;
@@ -299,14 +376,17 @@ __global__ void __launch_bounds__(kHopTile) k_hop_expand(HopArgs A) {
     return;
   }
   if (!(A.G.ordered || A.G.rank[w] < A.G.rank[x])) return;
-  const uint32_t cx = vcol(A.G, x), cv = vcol(A.G, v), cw = vcol(A.G, w);
+  const uint32_t ec = A.ecol[i];
+  const uint32_t cx = ec & 15u, cv = ec >> 4, cw = vcol(A.G, w);
   const uint32_t fin = A.first_hop ? (1u << cx) : ((1u << cx) | (1u << cv));
   const uint32_t fw = 1u << cw, fv = 1u << cv;
   if (fin & fw) return;  // the new vertex repeats a key colour: no colourful extension
   const uint32_t rr = A.record ? w : r;
   const uint64_t key = pack_key(x, w, rr, A.out_has_r, A.bits);
   if (KEYS) {
-    ht_insert(A.ht_key, A.ht_idx, A.ht_mask, A.ht_shift, key, A.n_keys, A.key_out);
+    const uint64_t h = ht_insert(A.ht_key, A.ht_idx, A.ht_mask, A.ht_shift, key, A.n_keys, A.key_out);
+    A.item_slot[item] = static_cast<uint32_t>(h);
+    A.item_col[item] = static_cast<uint16_t>(cx | (cv << 4) | (cw << 8));
     return;
   }
   const uint32_t oi = MODE == 2 ? ht_get(A.ht_key, A.ht_idx, A.ht_mask, A.ht_shift, key, A.n_keys, A.key_out,
@@ -595,6 +675,7 @@ struct Frontier {
   uint32_t P = 0;
   int has_r = 0;
   DBuf ht_key, ht_idx;  // hash table key -> entry (built by the hop that produced it)
+  long double ub = 1e30L;  // host upper bound of any row entry (1e30: unknown)
   uint64_t ht_mask = 0;
   int ht_shift = 64;
 };
@@ -680,6 +761,7 @@ struct CycleRunner {
   std::function<void(const uint64_t*, uint64_t*, uint64_t)> scan;  // exclusive scan of n+1
   DBuf sort_tmp;
   uint64_t mem_budget = 6ull << 30;  // bytes of per-hop scratch per batch
+  uint64_t max_deg = 0;               // largest degree of the graph (host bounds of plain hops)
   bool force = false;                 // single-anchor batch: no further split
   uint32_t h_mult = 1;                // Eq. 1 terms represented by each evaluated h
   uint32_t h_mult_t = 0;              // ... and terms equal to it with the pair keys swapped
@@ -771,25 +853,31 @@ struct CycleRunner {
     out.n = 0;
     if (in.n == 0) return true;
     DBuf work((in.n + 1) * 8), woff((in.n + 1) * 8), sstart(std::max<uint64_t>(in.n, 1) * 8);
+    DBuf ecol(std::max<uint64_t>(in.n, 1));
     MB_CUDA(cudaMemsetAsync(work.p, 0, (in.n + 1) * 8, stream));
     launch("cycle_hop_work", [&] {
       k_hop_work<<<grid_for(in.n, 256), 256, 0, stream>>>(in.key.as<uint64_t>(), in.n, in.has_r, bits, rel.off,
                                                           rel.adj, G.ordered, work.as<uint64_t>(),
-                                                          sstart.as<uint64_t>());
+                                                          sstart.as<uint64_t>(), G.chi, G.n, ecol.as<uint8_t>());
     });
+    // an output entry sums at most max_deg items x P_in entries of the input
+    // (plain hops; joined tables have no host bound: checked adds)
+    out.ub = (rel.pay || nt.kind) ? 1e30L : in.ub * static_cast<long double>(std::max<uint64_t>(max_deg, 1)) * in.P;
     scan(work.as<uint64_t>(), woff.as<uint64_t>(), in.n + 1);
     const uint64_t W = d2h(woff.as<uint64_t>() + in.n);
     if (W == 0) return true;
     // scratch: 2W hash slots (12 B), W keys, and at most W rows
-    batch_need = std::max<uint64_t>(batch_need, W * (out.P * 8ull + 40));
-    if (W * (out.P * 8ull + 40) > mem_budget && !force_hop) {
-      last_over = W * (out.P * 8ull + 40);
+    // (+ 5 B per item: the keys pass's slot and colour, + the tile starts)
+    batch_need = std::max<uint64_t>(batch_need, W * (out.P * 8ull + 47));
+    if (W * (out.P * 8ull + 47) > mem_budget && !force_hop) {
+      last_over = W * (out.P * 8ull + 47);
       return false;
     }
     // hash table: a power of two >= 2 W slots (load <= 1/2)
     int lg = 1;
     while ((1ull << lg) < 2 * W) ++lg;
     const uint64_t cap = 1ull << lg;
+    if (cap > (1ull << 31)) fail(kBudget, "cycle engine: a single hop needs more than 2^31 hash slots");
     out.ht_key.alloc(cap * 8);
     out.ht_idx.alloc(cap * 4);
     out.ht_mask = cap - 1;
@@ -827,6 +915,16 @@ struct CycleRunner {
     A.n_keys = reinterpret_cast<unsigned long long*>(nk.p);
     A.err = err;
     A.updates = upd;
+    const uint64_t ntiles = (W + kHopTile - 1) / kHopTile;
+    DBuf tstart((ntiles + 1) * 8), item_slot(W * 4), item_col(W * 2);
+    launch("cycle_tile_starts", [&] {
+      k_tile_starts<<<grid_for(ntiles + 1, 256), 256, 0, stream>>>(woff.as<uint64_t>(), in.n, W, ntiles,
+                                                                   tstart.as<uint64_t>());
+    });
+    A.tstart = tstart.as<uint64_t>();
+    A.item_slot = item_slot.as<uint32_t>(), A.item_col = item_col.as<uint16_t>();
+    A.ecol = ecol.as<uint8_t>();
+    A.unchecked = out.ub < 9.0e18L ? 1 : 0;
     static const bool dbg = std::getenv("MB_DEBUG_HOPS") != nullptr;
     // compulsory bytes: per item its neighbour id, colour and one probe
     // (8-byte key) per pass; per input entry its key, work offsets and row;
@@ -843,6 +941,10 @@ struct CycleRunner {
       out.pay.alloc(std::max<uint64_t>(out.n * out.P, 1) * 8);
       if (out.n) MB_CUDA(cudaMemsetAsync(out.pay.p, 0, out.n * out.P * 8, stream));
       A.row_out = out.pay.as<uint64_t>();
+      if (out.n && !rel.pay && !nt.kind)
+        launch("cycle_slot_index", [&] {
+          k_slot_to_index<<<grid_for(W, 256), 256, 0, stream>>>(A.item_slot, A.ht_idx, W);
+        }, W * 12);
       if (out.n)
         launch("cycle_hop_expand", [&] { k_hop_expand<1><<<grid_for(W, kHopTile), kHopTile, 0, stream>>>(A); },
                hop_bytes / 2 + out.n * (8 + 8ull * out.P));
@@ -888,7 +990,7 @@ struct CycleRunner {
 
   // Copies entries [i0, i0 + cnt) of a frontier (the slice stays sorted).
   void slice(const Frontier& f, uint64_t i0, uint64_t cnt, Frontier& a) {
-    a.s = f.s, a.P = f.P, a.has_r = f.has_r, a.n = cnt;
+    a.s = f.s, a.P = f.P, a.has_r = f.has_r, a.n = cnt, a.ub = f.ub;
     a.key.alloc(std::max<uint64_t>(cnt, 1) * 8), a.pay.alloc(std::max<uint64_t>(cnt * f.P, 1) * 8);
     MB_CUDA(cudaMemcpyAsync(a.key.p, f.key.as<uint64_t>() + i0, cnt * 8, cudaMemcpyDeviceToDevice, stream));
     MB_CUDA(cudaMemcpyAsync(a.pay.p, f.pay.as<uint64_t>() + i0 * f.P, cnt * f.P * 8, cudaMemcpyDeviceToDevice,
@@ -963,6 +1065,7 @@ struct CycleRunner {
     cur.P = use_start ? hn.P : 1;
     cur.n = nx;
     cur.has_r = 0;
+    cur.ub = use_start ? 1e30L : 1.0L;  // unannotated anchors start with the entry 1
     cur.key.alloc(std::max<uint32_t>(nx, 1) * 8);
     cur.pay.alloc(std::max<uint64_t>(static_cast<uint64_t>(nx) * cur.P, 1) * 8);
     launch("cycle_init", [&] {
