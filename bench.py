@@ -162,6 +162,10 @@ def dist_setup(args):
         import torch.distributed as dist
 
         backend = "nccl" if args.impl == "ours" else "gloo"
+        # MB_BENCH_ONE_GPU=1 (tests on a one-GPU box): every rank on cuda:0,
+        # gloo for the plumbing (NCCL refuses two ranks on one device)
+        if os.environ.get("MB_BENCH_ONE_GPU"):
+            backend, local = "gloo", 0
         if backend == "nccl":
             import torch
 
@@ -345,11 +349,76 @@ def overflow_arm(args, cfg, ws, rank, local, g, plan, dev):
         print(json.dumps(line), flush=True)
 
 
+def vertex_sharded_arm(args, cfg, ws, rank, local):
+    """--sharding vertex: STRONG scaling of one batch — every rank takes its
+    share of the data-graph vertices for the same colourings
+    (mb_count_colorful_sharded: leaf rows exchanged with an all-gather per leaf
+    table over NCCL, the root dealt over the ranks, partial counts all-gathered
+    and added with checked u64 arithmetic).  Host wall clock around the whole
+    call, max over ranks (the exchange runs on NCCL's stream)."""
+    import torch
+
+    import paper_1602_04478_b200 as mb
+    from paper_1602_04478_b200 import parallel
+
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    g = make_graph(mb, cfg["gen"], args.size)
+    plan = mb.QueryPlan(cfg["k"], cfg["query"])
+    k, n, nb = cfg["k"], g.num_vertices(), len(cfg["seeds"])
+    chis = np.stack([mb.random_coloring(g, k, s) for s in cfg["seeds"]])
+    cdev = "cpu" if ws > 1 and torch.distributed.get_backend() != "nccl" else dev
+
+    def step():
+        return parallel.distributed_count_vertex_sharded(g, plan, chis, device=cdev, exchange=True)
+
+    t0 = time.perf_counter()
+    counts0 = step()
+    first_call_s = time.perf_counter() - t0
+    for _ in range(max(args.warmup - 1, 0)):
+        step()
+    x0 = mb.engine_exchanged_bytes(g)
+    if ws > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        counts = step()
+    torch.cuda.synchronize()
+    dt = (time.perf_counter() - t0) / max(args.steps, 1)
+    clk = clocks.stop()
+    t = torch.tensor([dt], dtype=torch.float64, device=cdev)
+    if ws > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    dt = float(t.item())
+    assert np.array_equal(counts, counts0)
+    xb = (mb.engine_exchanged_bytes(g) - x0) // max(args.steps, 1)
+    line = {
+        "metric": "colorings/sec", "value": nb / dt, "unit": "colorings/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u64", "data": "synthetic",
+        "config": {"workload": cfg["name"] + (f"@size{args.size}" if args.size else ""), "n": n, "m": g.num_edges(),
+                   "k": k, "colorings_per_step": nb, "query_edges": cfg["query"],
+                   "parallelism": f"vertices sharded over {ws} GPU(s), leaf rows exchanged",
+                   "exchange_bytes_received_per_rank_per_step": int(xb), "first_call_s": first_call_s,
+                   "timing": "host wall clock around whole calls, max over ranks"},
+        "e2e": {"value": nb / dt, "unit": "colorings/s", "h2d_bytes_per_step": int(nb * n),
+                "d2h_bytes_per_step": int(8 * nb)},
+        "gpu_launches": None, "clocks": clk, "counts_first3": [int(x) for x in counts0[:3]],
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
 def our_arm(args, cfg, ws, rank, local):
     import torch
 
     import paper_1602_04478_b200 as mb
 
+    if args.sharding == "vertex":
+        return vertex_sharded_arm(args, cfg, ws, rank, local)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     g = make_graph(mb, cfg["gen"], args.size)
@@ -497,6 +566,9 @@ def main():
                     help="size of the bounded sample the reference (and the same-input GPU run) is timed on")
     ap.add_argument("--overflow-colorings", type=int, default=4,
                     help="colourings resolved per step on workloads whose count overflows u64 (configs 2, 4)")
+    ap.add_argument("--sharding", choices=["colorings", "vertex"], default="colorings",
+                    help="multi-GPU layout: colourings dealt over ranks (weak scaling, the default) or the "
+                         "data-graph vertices of one batch sharded with leaf-row exchange (strong scaling)")
     ap.add_argument("--size", type=int, default=None,
                     help="override the generator size (n, or the R-MAT scale): supplementary reduced runs of "
                          "configs 2-4, whose full sizes exceed u64 counts or HBM (DESIGN.md)")

@@ -34,7 +34,12 @@ SCALE = {"ns": 1e-6, "us": 1e-3, "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "s"
 def main():
     rep, tag, note = sys.argv[1], sys.argv[2], sys.argv[3]
     names = [a.split("=", 1) for a in sys.argv[4:]]
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    # REPORT may also be the `ncu -i ... --page raw --csv` dump of a report that
+    # stayed on the GPU box (full reports with sources exceed gpurun's copy-back limit)
+    if rep.endswith(".csv"):
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     hdr, units, data = rows[0], rows[1], rows[2:]
     col = {h: i for i, h in enumerate(hdr)}
