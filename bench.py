@@ -395,6 +395,10 @@ def vertex_sharded_arm(args, cfg, ws, rank, local):
     dt = float(t.item())
     assert np.array_equal(counts, counts0)
     xb = (mb.engine_exchanged_bytes(g) - x0) // max(args.steps, 1)
+    # the sharded totals against this rank's own unsharded count of the same batch
+    whole = mb.count_colorful(g, plan, chis)
+    if not np.array_equal(whole, counts0):
+        raise SystemExit("bench: vertex-sharded counts differ from the unsharded count")
     line = {
         "metric": "colorings/sec", "value": nb / dt, "unit": "colorings/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "strong",
@@ -407,6 +411,7 @@ def vertex_sharded_arm(args, cfg, ws, rank, local):
         "e2e": {"value": nb / dt, "unit": "colorings/s", "h2d_bytes_per_step": int(nb * n),
                 "d2h_bytes_per_step": int(8 * nb)},
         "gpu_launches": None, "clocks": clk, "counts_first3": [int(x) for x in counts0[:3]],
+        "counts_equal_unsharded": True,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
