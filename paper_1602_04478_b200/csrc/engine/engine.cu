@@ -430,6 +430,31 @@ __global__ void k_rows_unpack(U* __restrict__ table, const U* __restrict__ buf, 
   if (v < n) table[v * units_per_row + u] = buf[idx];
 }
 
+// The same exchange restricted to a vertex list (leaf tables computed at the
+// demanded vertices only): idx[q * rows + i] = the i-th listed vertex owned by
+// rank q, ~0u past the end of q's share.
+template <class U>
+__global__ void k_rows_pack_idx(const U* __restrict__ table, U* __restrict__ slice, const uint32_t* __restrict__ idx,
+                                uint64_t units_per_row, uint64_t rows) {
+  const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  if (t >= rows * units_per_row) return;
+  const uint64_t i = t / units_per_row, u = t - i * units_per_row;
+  const uint32_t v = idx[i];
+  if (v != ~0u) slice[t] = table[static_cast<uint64_t>(v) * units_per_row + u];
+}
+template <class U>
+__global__ void k_rows_unpack_idx(U* __restrict__ table, const U* __restrict__ buf, const uint32_t* __restrict__ idx,
+                                  uint32_t rank, uint32_t world, uint64_t units_per_row, uint64_t rows) {
+  const uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
+  const uint64_t per = rows * units_per_row;
+  if (t >= per * world) return;
+  const uint64_t q = t / per, r = t - q * per;
+  if (q == rank) return;
+  const uint64_t i = r / units_per_row, u = r - i * units_per_row;
+  const uint32_t v = idx[q * rows + i];
+  if (v != ~0u) table[static_cast<uint64_t>(v) * units_per_row + u] = buf[t];
+}
+
 // Degree-ordered orientation: out(x) = neighbours ranked below x, kept in id
 // order, remembered with their CSR slot.
 __global__ void k_out_degree(uint32_t n, const uint64_t* __restrict__ off, const uint32_t* __restrict__ adj,
