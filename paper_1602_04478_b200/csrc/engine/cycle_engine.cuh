@@ -358,6 +358,9 @@ __global__ void __launch_bounds__(kHopTile) k_hop_expand(HopArgs A) {
     if ((threadIdx.x & 31) == static_cast<unsigned>(__ffs(am) - 1) && tot) atomicAdd(A.updates, static_cast<u64>(tot));
     return;
   }
+  // accumulate pass: items the keys pass dropped (no slot) are done; live ones
+  // carry their row index and colours
+  if (MODE == 1 && A.item_slot[item] == ~0u) return;
   uint32_t x, v, r;
   unpack_key(A.key_in[i], A.in_has_r, A.bits, x, v, r);
   if (MODE == 0) A.item_slot[item] = ~0u;  // until the item proves live below
@@ -377,7 +380,8 @@ __global__ void __launch_bounds__(kHopTile) k_hop_expand(HopArgs A) {
   }
   if (!(A.G.ordered || A.G.rank[w] < A.G.rank[x])) return;
   const uint32_t ec = A.ecol[i];
-  const uint32_t cx = ec & 15u, cv = ec >> 4, cw = vcol(A.G, w);
+  // (the accumulate pass takes the neighbour's colour from the keys pass)
+  const uint32_t cx = ec & 15u, cv = ec >> 4, cw = MODE == 1 ? A.item_col[item] >> 8 : vcol(A.G, w);
   const uint32_t fin = A.first_hop ? (1u << cx) : ((1u << cx) | (1u << cv));
   const uint32_t fw = 1u << cw, fv = 1u << cv;
   if (fin & fw) return;  // the new vertex repeats a key colour: no colourful extension
@@ -389,9 +393,10 @@ __global__ void __launch_bounds__(kHopTile) k_hop_expand(HopArgs A) {
     A.item_col[item] = static_cast<uint16_t>(cx | (cv << 4) | (cw << 8));
     return;
   }
+  // accumulate pass: the row index the keys pass (and k_slot_to_index) left
   const uint32_t oi = MODE == 2 ? ht_get(A.ht_key, A.ht_idx, A.ht_mask, A.ht_shift, key, A.n_keys, A.key_out,
                                           A.row_out, A.P_out)
-                                  : ht_find(A.ht_key, A.ht_idx, A.ht_mask, A.ht_shift, key);
+                                  : A.item_slot[item];
   if (oi == ~0u) {
     atomicOr(A.err, 64);
     return;
@@ -941,7 +946,7 @@ struct CycleRunner {
       out.pay.alloc(std::max<uint64_t>(out.n * out.P, 1) * 8);
       if (out.n) MB_CUDA(cudaMemsetAsync(out.pay.p, 0, out.n * out.P * 8, stream));
       A.row_out = out.pay.as<uint64_t>();
-      if (out.n && !rel.pay && !nt.kind)
+      if (out.n)
         launch("cycle_slot_index", [&] {
           k_slot_to_index<<<grid_for(W, 256), 256, 0, stream>>>(A.item_slot, A.ht_idx, W);
         }, W * 12);
