@@ -110,14 +110,17 @@ int mb_count_colorful_shard(mb_graph* g, mb_plan* p, const uint8_t* chi, int nco
  * reference's BSP rounds ship table entries to the owner of their key vertex
  * (redistribute / extend, runtime.cpp:94-114, 173-202); here each rank packs
  * its rows into slice `rank` of a DEVICE buffer of `world` slices of
- * `bytes_per_rank` bytes and calls `allgather(ctx, buf, bytes_per_rank)`, which
- * must fill the other slices with the other ranks' (an in-place all-gather:
- * ncclAllGather on the caller's communicator, or a host-staged gather) and
- * return 0 once the data is in place.  Every rank makes the same sequence of
- * calls.  A root 3-cycle block with a scalar output is dealt over the ranks
- * by warp batch of oriented edges, a root cycle block by anchor vertex, a
- * root leaf block by vertex; *split as above. */
-typedef int (*mb_allgather_fn)(void* ctx, void* dev_buf, uint64_t bytes_per_rank);
+ * `bytes_per_rank` bytes and calls `allgather(ctx, buf, bytes_per_rank,
+ * stream)`, which must fill the other slices with the other ranks' (an
+ * in-place all-gather).  `stream` is the engine's cudaStream_t: the packed
+ * rows are ready in stream order on it, and the callback must leave the
+ * gathered buffer ready in stream order on it — enqueue ncclAllGather on that
+ * stream and return (nothing blocks the host), or synchronise it, gather
+ * through the host and copy back.  Returns 0 on success.  Every rank makes the
+ * same sequence of calls.  A root 3-cycle block with a scalar output is dealt
+ * over the ranks by warp batch of oriented edges, a root cycle block by anchor
+ * vertex, a root leaf block by vertex; *split as above. */
+typedef int (*mb_allgather_fn)(void* ctx, void* dev_buf, uint64_t bytes_per_rank, void* cuda_stream);
 int mb_count_colorful_sharded(mb_graph* g, mb_plan* p, const uint8_t* chi, int ncol, int engine,
                               int rank, int world, mb_allgather_fn allgather, void* ctx,
                               uint64_t* partial, int* split);

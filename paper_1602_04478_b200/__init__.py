@@ -89,8 +89,8 @@ _ERRORS = {c.code: c for c in (ParseError, TreewidthError, CountOverflowError, B
                                 SchemaError, ContractError, SpecError, CudaError)}
 
 
-# mb_allgather_fn (include/motif_b200.h): int (*)(void* ctx, void* dev_buf, uint64_t bytes_per_rank)
-ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64)
+# mb_allgather_fn (include/motif_b200.h): int (*)(void* ctx, void* dev_buf, uint64_t bytes_per_rank, void* stream)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p)
 
 
 def _load() -> C.CDLL:
@@ -377,8 +377,9 @@ def count_colorful_sharded(g: DataGraph, plan: QueryPlan, chi: np.ndarray, rank:
                            engine: int = DB) -> tuple[np.ndarray, bool]:
     """mb_count_colorful_sharded: this rank's partial counts with the leaf
     blocks computed for its own vertices and their rows exchanged through
-    ``allgather(dev_ptr, bytes_per_rank)`` (an in-place all-gather over a
-    device buffer of ``world`` slices; see parallel.make_allgather)."""
+    ``allgather(dev_ptr, bytes_per_rank, cuda_stream)`` (an in-place all-gather
+    over a device buffer of ``world`` slices, in stream order on the engine's
+    stream; see parallel.make_allgather)."""
     a = np.ascontiguousarray(np.atleast_2d(chi), dtype=np.uint8)
     if a.shape[1] != g.num_vertices():
         raise SpecError("colouring length != number of vertices")
@@ -386,9 +387,9 @@ def count_colorful_sharded(g: DataGraph, plan: QueryPlan, chi: np.ndarray, rank:
     split = C.c_int()
     failure: list[BaseException] = []
 
-    def _cb(_ctx, ptr, nbytes):
+    def _cb(_ctx, ptr, nbytes, stream):
         try:
-            allgather(int(ptr), int(nbytes))
+            allgather(int(ptr), int(nbytes), int(stream or 0))
             return 0
         except BaseException as e:  # surfaces as CudaError below, with the cause attached
             failure.append(e)

@@ -284,8 +284,8 @@ int mb_count_colorful_sharded(mb_graph* g, mb_plan* p, const uint8_t* chi, int n
     auto& eng = engine_for(g, p);
     eng.set_shard(static_cast<uint32_t>(rank), static_cast<uint32_t>(world));
     if (world > 1)
-      eng.set_exchange([allgather, ctx](void* buf, uint64_t bytes) {
-        if (allgather(ctx, buf, bytes) != 0) mb::fail(mb::kCuda, "table exchange (all-gather callback) failed");
+      eng.set_exchange([allgather, ctx](void* buf, uint64_t bytes, void* stream) {
+        if (allgather(ctx, buf, bytes, stream) != 0) mb::fail(mb::kCuda, "table exchange (all-gather callback) failed");
       });
     auto reset = [&] {
       eng.set_exchange(nullptr);

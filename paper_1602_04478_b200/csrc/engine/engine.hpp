@@ -85,10 +85,12 @@ class GpuEngine {
   // this rank's vertices, packs them into slice `rank` of a device buffer of
   // `world` equal slices and calls the exchange, which must fill the other
   // slices with the other ranks' rows (an in-place all-gather: NCCL on
-  // NVLink, or staged through the host); the rows are then unpacked so every
-  // rank holds the whole table again.  Blocks above the leaves read whole
-  // tables, so only these rows ever cross ranks.
-  using AllGather = std::function<void(void* dev_buf, uint64_t bytes_per_rank)>;
+  // NVLink, or staged through the host), in stream order on the engine's
+  // stream (passed along: a collective enqueued on it needs no host
+  // synchronisation); the rows are then unpacked so every rank holds the
+  // whole table again.  Blocks above the leaves read whole tables, so only
+  // these rows ever cross ranks.
+  using AllGather = std::function<void(void* dev_buf, uint64_t bytes_per_rank, void* cuda_stream)>;
   void set_exchange(AllGather fn);
   uint64_t exchanged_bytes() const;  // bytes received through the exchange so far
 

@@ -136,35 +136,42 @@ def gather_slices(slices: Sequence[np.ndarray]) -> np.ndarray:
 
 
 def make_allgather(dist, world: int, rank: int, device=None):
-    """The ``allgather(dev_ptr, bytes_per_rank)`` callback of
+    """The ``allgather(dev_ptr, bytes_per_rank, cuda_stream)`` callback of
     count_colorful_sharded over torch.distributed: the engine has packed this
-    rank's rows into slice ``rank`` of the device buffer; on return every slice
-    holds its rank's rows.  NCCL gathers in place on the device (NVLink);
-    other backends stage the slices through host memory."""
+    rank's rows into slice ``rank`` of the device buffer (ready in stream order
+    on its stream); on return every slice holds its rank's rows, again in
+    stream order on that stream.  NCCL gathers in place on the device (NVLink)
+    with the engine's stream current, so nothing blocks the host; other
+    backends synchronise and stage the slices through host memory."""
     import torch
 
     nccl = dist.get_backend() == "nccl"
     if device is None:
         device = torch.device("cuda", torch.cuda.current_device())
-
     on_host = torch.device(device).type == "cpu"  # CPU tests: the buffer is host memory
 
-    def allgather(ptr: int, nbytes: int) -> None:
+    def allgather(ptr: int, nbytes: int, stream: int = 0) -> None:
         if on_host:
             import ctypes
 
             buf = torch.from_numpy(np.ctypeslib.as_array((ctypes.c_uint8 * (nbytes * world)).from_address(ptr)))
-        else:
-            buf = torch.as_tensor(_DeviceBytes(ptr, nbytes * world), device=device)
-        mine = buf[rank * nbytes:(rank + 1) * nbytes]
-        if nccl:
-            dist.all_gather_into_tensor(buf, mine.clone())
-        else:
             parts = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(world)]
-            dist.all_gather(parts, mine.cpu())
+            dist.all_gather(parts, buf[rank * nbytes:(rank + 1) * nbytes].clone())
             buf.copy_(torch.from_numpy(gather_slices([p.numpy() for p in parts])))
-        if not on_host:
-            torch.cuda.synchronize(device)
+            return
+        ext = torch.cuda.ExternalStream(stream, device=device) if stream else torch.cuda.current_stream(device)
+        with torch.cuda.stream(ext):
+            buf = torch.as_tensor(_DeviceBytes(ptr, nbytes * world), device=device)
+            mine = buf[rank * nbytes:(rank + 1) * nbytes]
+            if nccl:
+                # NCCL orders itself after the current stream (the engine's) and
+                # the current stream after the collective: asynchronous
+                dist.all_gather_into_tensor(buf, mine.clone())
+            else:
+                parts = [torch.empty(nbytes, dtype=torch.uint8) for _ in range(world)]
+                dist.all_gather(parts, mine.cpu())  # .cpu() waits for the packed rows
+                buf.copy_(torch.from_numpy(gather_slices([p.numpy() for p in parts])))
+                ext.synchronize()  # the staging tensor must outlive the copy
 
     return allgather
 

@@ -131,7 +131,7 @@ def _shard_worker(rank, world, port, results):
         nbytes = 4096 + 16
         xbuf = np.zeros(world * nbytes, np.uint8)
         xbuf[rank * nbytes:(rank + 1) * nbytes] = (np.arange(nbytes) * (rank + 3) + rank) % 251
-        parallel.make_allgather(dist, world, rank, device="cpu")(xbuf.ctypes.data, nbytes)
+        parallel.make_allgather(dist, world, rank, device="cpu")(xbuf.ctypes.data, nbytes, 0)
         xok = all(np.array_equal(xbuf[q * nbytes:(q + 1) * nbytes], (np.arange(nbytes) * (q + 3) + q) % 251)
                   for q in range(world))
         results[rank] = ([int(x) for x in got], want, over, over1, xok)

@@ -16,6 +16,6 @@ for name, (k, q) in qs.items():
     # one rank of a 2-rank sharded count with a no-op exchange (rows of the other rank stay stale:
     # the partial is meaningless, the kernels and index arithmetic are what is checked)
     try:
-        mb.count_colorful_sharded(g, plan, chis, 1, 2, lambda ptr, nbytes: None)
+        mb.count_colorful_sharded(g, plan, chis, 1, 2, lambda ptr, nbytes, stream: None)
     except mb.MotifError as e:
         print("  sharded dry run:", type(e).__name__)
