@@ -92,9 +92,17 @@ int mb_plan_score(const mb_plan* p, int idx, int* score3);
  * HOST memory; the graph, colourings and results cross PCIe inside the call. */
 int mb_count_colorful(mb_graph* g, mb_plan* p, const uint8_t* chi, int ncol, int engine,
                       uint64_t* out);
-/* Same, colourings generated from seeds with random_coloring(n, k, seed). */
+/* Same, colourings generated from seeds with random_coloring(n, k, seed) ON
+ * THE DEVICE: seeds in, counts out, no colouring crosses PCIe. */
 int mb_count_colorful_seeds(mb_graph* g, mb_plan* p, const uint64_t* seeds, int ncol, int engine,
                             uint64_t* out);
+/* The colourings random_coloring(n, k, seeds[i]) as the DEVICE generates them
+ * for mb_count_colorful_seeds / mb_estimate (one warp per colouring runs the
+ * mt19937_64 stream; bit-identical to mb_random_coloring), copied to host
+ * memory (n bytes per seed): for tests and callers that want to inspect them.
+ * limit = 0 uses the reference's rejection limit 2^64 - 1 - (2^64 - 1) % k. */
+int mb_device_random_colorings(mb_graph* g, int k, const uint64_t* seeds, int ncol, uint64_t limit,
+                               uint8_t* out);
 /* Vertex-sharded count (one rank of a multi-GPU job; the
  * reference's BspExecutor over Partition, runtime.cpp:11-25, 297-324): this
  * rank's partial count of each colouring, the matches of the root block

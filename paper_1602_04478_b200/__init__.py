@@ -42,7 +42,7 @@ __all__ = [
     "MotifError", "ParseError", "TreewidthError", "CountOverflowError", "BudgetError",
     "SchemaError", "ContractError", "SpecError", "CudaError",
     "DataGraph", "QueryPlan", "EstimateReport", "Partition", "load_edge_list", "degree_rank",
-    "random_coloring", "derive_seed", "count_colorful", "count_colorful_shard", "count_colorful_sharded", "estimate", "automorphism_count",
+    "random_coloring", "derive_seed", "count_colorful", "count_colorful_shard", "count_colorful_sharded", "device_random_colorings", "estimate", "automorphism_count",
     "normalization_factor", "coefficient_of_variation", "estimate_from_counts", "PS", "DB", "lib",
 ]
 
@@ -133,6 +133,7 @@ def _load() -> C.CDLL:
         "mb_count_colorful": (C.c_int, [P, P, u8p, C.c_int, C.c_int, u64p]),
         "mb_count_colorful_seeds": (C.c_int, [P, P, u64p, C.c_int, C.c_int, u64p]),
         "mb_count_colorful_device": (C.c_int, [P, P, C.c_void_p, C.c_int, u64p]),
+        "mb_device_random_colorings": (C.c_int, [P, C.c_int, u64p, C.c_int, C.c_uint64, u8p]),
         "mb_count_colorful_shard": (C.c_int, [P, P, u8p, C.c_int, C.c_int, C.c_int, C.c_int, u64p,
                                               C.POINTER(C.c_int)]),
         "mb_count_colorful_sharded": (C.c_int, [P, P, u8p, C.c_int, C.c_int, C.c_int, C.c_int, ALLGATHER_FN,
@@ -355,6 +356,15 @@ def count_colorful_seeds(g: DataGraph, plan: QueryPlan, seeds: Iterable[int], en
     out = np.zeros(len(s), dtype=np.uint64)
     _check(lib.mb_count_colorful_seeds(g.handle, plan.handle, _ptr(s, C.c_uint64), len(s), engine,
                                        _ptr(out, C.c_uint64)))
+    return out
+
+
+def device_random_colorings(g: DataGraph, k: int, seeds: Iterable[int], limit: int = 0) -> np.ndarray:
+    """random_coloring(n, k, seed) of every seed as the device generates them
+    for count_colorful_seeds / estimate (mb_device_random_colorings); (len(seeds), n)."""
+    s = np.ascontiguousarray(list(seeds), dtype=np.uint64)
+    out = np.zeros((len(s), g.num_vertices()), dtype=np.uint8)
+    _check(lib.mb_device_random_colorings(g.handle, k, _ptr(s, C.c_uint64), len(s), limit, _ptr(out, C.c_uint8)))
     return out
 
 

@@ -227,33 +227,32 @@ int mb_count_colorful(mb_graph* g, mb_plan* p, const uint8_t* chi, int ncol, int
   });
 }
 
+// colourings per device call of the seeded entry points
+static int seed_batch(uint32_t n) {
+  return static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>(256, (1ull << 30) / std::max<uint32_t>(n, 1))));
+}
+
 int mb_count_colorful_seeds(mb_graph* g, mb_plan* p, const uint64_t* seeds, int ncol, int engine,
                             uint64_t* out) {
   return guarded([&] {
     if (engine != 0 && engine != 1) mb::fail(mb::kSpec, "engine must be 0 (PS) or 1 (DB)");
     if (ncol < 0) mb::fail(mb::kSpec, "negative colouring count");
     auto& eng = engine_for(g, p);
-    const uint32_t n = g->g.n;
-    // bounded batches (as mb_estimate): at most 64 colourings or 256 MB of
-    // host colours per device call, generated by a fixed pool of threads
-    const int batch = static_cast<int>(
-        std::max<uint64_t>(1, std::min<uint64_t>(64, (256ull << 20) / std::max<uint32_t>(n, 1))));
-    const int nthreads = static_cast<int>(std::max(1u, std::min(16u, std::thread::hardware_concurrency())));
-    std::vector<uint8_t> chi;
-    for (int c0 = 0; c0 < ncol; c0 += batch) {
-      const int nb = std::min(batch, ncol - c0);
-      chi.resize(static_cast<size_t>(n) * nb);
-      std::vector<std::thread> ts;
-      for (int t = 0; t < std::min(nthreads, nb); ++t)
-        ts.emplace_back([&, t] {
-          for (int c = t; c < nb; c += nthreads) {
-            const auto col = mb::random_coloring(n, p->q.k, seeds[c0 + c]);
-            std::memcpy(chi.data() + static_cast<size_t>(c) * n, col.data(), n);
-          }
-        });
-      for (auto& t : ts) t.join();
-      eng.count(chi.data(), nb, true, out + c0);
+    // the colourings are generated on the device (GpuEngine::count_seeds), in
+    // bounded batches: at most 256 colourings or 1 GB of colours per call
+    eng.count_seeds_batched(seeds, static_cast<uint64_t>(ncol), seed_batch(g->g.n), out);
+  });
+}
+
+int mb_device_random_colorings(mb_graph* g, int k, const uint64_t* seeds, int ncol, uint64_t limit, uint8_t* out) {
+  return guarded([&] {
+    if (ncol < 0) mb::fail(mb::kSpec, "negative colouring count");
+    if (!g->eng) {
+      g->eng = std::make_unique<mb::GpuEngine>(g->g, -1);
+      g->eng->enable_timing(g->timing);
+      g->bound = nullptr;
     }
+    g->eng->random_colorings(k, seeds, ncol, limit, out);
   });
 }
 
@@ -348,19 +347,11 @@ int mb_estimate(mb_graph* g, mb_plan* p, int engine, uint64_t trials, uint64_t s
     const double norm = mb::normalization_factor(p->q.k);
     auto& eng = engine_for(g, p);
     const uint32_t n = g->g.n;
-    // Batches of colourings: host generation overlaps nothing yet; each batch
-    // is one device call.
-    const uint64_t batch = std::max<uint64_t>(1, std::min<uint64_t>(64, (256ull << 20) / std::max<uint32_t>(n, 1)));
-    std::vector<uint8_t> chi;
-    for (uint64_t t0 = 0; t0 < trials; t0 += batch) {
-      const uint64_t nb = std::min(batch, trials - t0);
-      chi.resize(nb * n);
-      for (uint64_t i = 0; i < nb; ++i) {
-        const auto c = mb::random_coloring(n, p->q.k, mb::derive_seed(seed, t0 + i));
-        std::memcpy(chi.data() + i * n, c.data(), n);
-      }
-      eng.count(chi.data(), static_cast<int>(nb), true, per_trial + t0);
-    }
+    // Trial i's colouring is random_coloring(n, k, derive_seed(seed, i))
+    // (estimate.cpp:108-117), generated on the device in bounded batches
+    std::vector<uint64_t> seeds(trials);
+    for (uint64_t i = 0; i < trials; ++i) seeds[i] = mb::derive_seed(seed, i);
+    eng.count_seeds_batched(seeds.data(), trials, seed_batch(n), per_trial);
     (void)norm;
     *aut = mb::automorphism_count(p->q);
     const int rc = mb_estimate_from_counts(p->q.k, *aut, per_trial, trials, mean, cv, subgraph);

@@ -317,6 +317,82 @@ __global__ void k_recolor(uint32_t n, int C, const uint8_t* __restrict__ in, uin
   reinterpret_cast<unsigned long long*>(out)[v] = cols;
 }
 
+// Seeded colourings on the device, bit-identical to random_coloring
+// (reference graph.cpp:142-151: std::mt19937_64(seed), one draw per vertex in
+// vertex order, draws >= limit = 2^64 - 1 - (2^64 - 1) % k rejected, colour
+// 1 + x % k).  One warp per colouring: the 312-word MT state lives in shared
+// memory and is regenerated 312 outputs at a time — the recurrence
+// x[i] <- x[i+156] ^ twist(x[i], x[i+1]) is evaluated 32 elements per step,
+// first i < 156 (reads only old words), then i >= 156 (reads the new lower
+// half), which is the sequential order's data flow — then tempered, reduced
+// mod k by a multiply-high, and compacted over rejections with a ballot so
+// the vertex order is exact.  estimate()'s trials therefore never cross PCIe:
+// seeds in, counts out.
+__device__ __forceinline__ uint64_t mt_temper(uint64_t x) {
+  x ^= (x >> 29) & 0x5555555555555555ull;
+  x ^= (x << 17) & 0x71D67FFFEDA60000ull;
+  x ^= (x << 37) & 0xFFF7EEE000000000ull;
+  x ^= x >> 43;
+  return x;
+}
+__global__ void __launch_bounds__(32) k_random_colorings(const uint64_t* __restrict__ seeds, uint32_t n, uint32_t k,
+                                                         uint64_t limit, uint8_t* __restrict__ out) {
+  constexpr int NN = 312, MM = 156;
+  constexpr uint64_t UM = 0xFFFFFFFF80000000ull, LM = 0x7FFFFFFFull, MATRIX_A = 0xB5026F5AA96619E9ull;
+  __shared__ uint64_t mt[NN];
+  const uint32_t lane = threadIdx.x;
+  uint8_t* chi = out + static_cast<uint64_t>(blockIdx.x) * n;
+  if (lane == 0) {
+    uint64_t x = seeds[blockIdx.x];
+    mt[0] = x;
+    for (int i = 1; i < NN; ++i) {
+      x = 6364136223846793005ull * (x ^ (x >> 62)) + static_cast<uint64_t>(i);
+      mt[i] = x;
+    }
+  }
+  __syncwarp();
+  const uint64_t magic = k > 1 ? ~0ull / k : 0;  // floor((2^64 - 1) / k): quotient estimate low by at most 1
+  uint32_t v = 0;  // next vertex
+  while (v < n) {
+    // regenerate the state
+    for (int half = 0; half < 2; ++half) {
+      const int lo = half * MM, hi = lo + MM;
+      for (int base = lo; base < hi; base += 32) {
+        const int i = base + lane;
+        uint64_t nx = 0;
+        if (i < hi) {
+          const uint64_t y = (mt[i] & UM) | (mt[(i + 1) % NN] & LM);
+          nx = mt[(i + MM) % NN] ^ (y >> 1) ^ ((y & 1ull) ? MATRIX_A : 0ull);
+        }
+        __syncwarp();  // every lane has read the old words of this step
+        if (i < hi) mt[i] = nx;
+        __syncwarp();
+      }
+    }
+    // consume the 312 outputs in order
+    for (int base = 0; base < NN && v < n; base += 32) {
+      const int i = base + lane;
+      uint64_t x = i < NN ? mt_temper(mt[i]) : ~0ull;
+      const bool ok = i < NN && x < limit;
+      const unsigned acc = __ballot_sync(0xffffffffu, ok);
+      const uint32_t dst = v + __popc(acc & ((1u << lane) - 1u));
+      if (ok && dst < n) {
+        uint64_t r = x;
+        if (k > 1) {
+          const uint64_t q = __umul64hi(x, magic);
+          r = x - q * k;
+          if (r >= k) r -= k;
+          if (r >= k) r -= k;
+        } else {
+          r = 0;
+        }
+        chi[dst] = static_cast<uint8_t>(1 + r);
+      }
+      v += __popc(acc);
+    }
+  }
+}
+
 // The kChiStride colours of vertex v (one 8-byte load) and colour slot c of them.
 __device__ __forceinline__ uint64_t load_colors(const uint8_t* chi, uint32_t v) {
   return __ldg(reinterpret_cast<const unsigned long long*>(chi) + v);

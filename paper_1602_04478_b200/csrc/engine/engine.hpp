@@ -53,6 +53,16 @@ class GpuEngine {
   // Colourful count for each colouring.  `chi` holds `count` colourings of n
   // vertices each, colours 1..k, in host memory (host=true) or device memory.
   void count(const uint8_t* chi, int count_colorings, bool host, uint64_t* out);
+  // The same for the colourings random_coloring(n, k, seeds[i]), generated on
+  // the device (k_random_colorings): nothing but the seeds and the counts
+  // crosses PCIe.  `count_colorings` is bounded by the caller (n bytes each).
+  void count_seeds(const uint64_t* seeds, int count_colorings, uint64_t* out);
+  // ... for any number of seeds, `batch` colourings per device call, batch i + 1
+  // generated on a side stream while batch i is counted.
+  void count_seeds_batched(const uint64_t* seeds, uint64_t total, int batch, uint64_t* out);
+  // The device-generated colourings themselves (tests): n bytes per seed into
+  // host memory; limit = 0 uses the reference's rejection limit.
+  void random_colorings(int k, const uint64_t* seeds, int count_colorings, uint64_t limit, uint8_t* out_host);
 
   // Drops plan-derived graph structures (triangle list); the next count
   // rebuilds them.  Used by the benchmark to keep that work inside a step.

@@ -112,3 +112,40 @@ def test_cycle_plans_every_tree(mb, reference, name):
     for t in range(plan.num_trees()):
         plan.use_tree(t)
         assert mb.count_colorful(g, plan, chi) == want, plan.canonical(t)
+
+
+def test_device_colourings_are_the_reference_colourings(mb):
+    """count_colorful_seeds / estimate generate their colourings on the device
+    (k_random_colorings: one warp per mt19937_64 stream).  They must be the
+    reference's random_coloring byte for byte (graph.cpp:142-151), for sizes
+    around the generator's 312-word state and every k, and also when draws are
+    rejected: with the rejection limit forced to 2^63 about half of the draws
+    are skipped, and the expected colours follow from the raw stream of the
+    oracle's generator (pinned to std::mt19937_64 in tests/test_oracle.py)."""
+    from oracle import Oracle
+
+    O = Oracle()
+    for n in (1, 311, 312, 313, 1000, 100003):
+        g = mb.DataGraph.from_edges(n, np.zeros((0, 2), dtype=np.int64))
+        for k in (1, 2, 3, 6, 7, 10, 16, 32):
+            seeds = [7, 100, 2**63 + 5, 0]
+            got = mb.device_random_colorings(g, k, seeds)
+            for i, s in enumerate(seeds):
+                assert np.array_equal(got[i], mb.random_coloring(g, k, s)), (n, k, s)
+        limit = 1 << 63
+        seeds = [3, 4]
+        got = mb.device_random_colorings(g, 6, seeds, limit=limit)
+        for i, s in enumerate(seeds):
+            raw = O.mt64(s, 4 * n + 64)
+            acc = raw[raw < np.uint64(limit)][:n]
+            assert len(acc) == n
+            assert np.array_equal(got[i], (1 + acc % np.uint64(6)).astype(np.uint8)), (n, s)
+
+
+def test_seeded_counts_equal_counts_of_host_colourings(mb):
+    g = mb.DataGraph.chung_lu(3000, 2.1, 8.0, 11)
+    seeds = list(range(40, 53))  # 13: one full batch of 8 and a partial one
+    for k, q in ((6, [(0, 1), (1, 2), (2, 0), (1, 3), (3, 2), (2, 4), (4, 5)]), (5, [(i, (i + 1) % 5) for i in range(5)])):
+        plan = mb.QueryPlan(k, q)
+        chis = np.stack([mb.random_coloring(g, k, s) for s in seeds])
+        assert np.array_equal(mb.count_colorful_seeds(g, plan, seeds), mb.count_colorful(g, plan, chis))
