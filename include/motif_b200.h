@@ -97,7 +97,7 @@ int mb_count_colorful(mb_graph* g, mb_plan* p, const uint8_t* chi, int ncol, int
 int mb_count_colorful_seeds(mb_graph* g, mb_plan* p, const uint64_t* seeds, int ncol, int engine,
                             uint64_t* out);
 /* The colourings random_coloring(n, k, seeds[i]) as the DEVICE generates them
- * for mb_count_colorful_seeds / mb_estimate (one warp per colouring runs the
+ * for mb_count_colorful_seeds / mb_estimate (one CTA per colouring runs the
  * mt19937_64 stream; bit-identical to mb_random_coloring), copied to host
  * memory (n bytes per seed): for tests and callers that want to inspect them.
  * limit = 0 uses the reference's rejection limit 2^64 - 1 - (2^64 - 1) % k. */

@@ -320,13 +320,13 @@ __global__ void k_recolor(uint32_t n, int C, const uint8_t* __restrict__ in, uin
 // Seeded colourings on the device, bit-identical to random_coloring
 // (reference graph.cpp:142-151: std::mt19937_64(seed), one draw per vertex in
 // vertex order, draws >= limit = 2^64 - 1 - (2^64 - 1) % k rejected, colour
-// 1 + x % k).  One warp per colouring: the 312-word MT state lives in shared
-// memory and is regenerated 312 outputs at a time — the recurrence
-// x[i] <- x[i+156] ^ twist(x[i], x[i+1]) is evaluated 32 elements per step,
+// 1 + x % k).  One 160-thread CTA per colouring: the 312-word MT state lives in
+// shared memory and is regenerated 312 outputs at a time — the recurrence
+// x[i] <- x[i+156] ^ twist(x[i], x[i+1]) is evaluated a half state per step,
 // first i < 156 (reads only old words), then i >= 156 (reads the new lower
 // half), which is the sequential order's data flow — then tempered, reduced
-// mod k by a multiply-high, and compacted over rejections with a ballot so
-// the vertex order is exact.  estimate()'s trials therefore never cross PCIe:
+// mod k by a multiply-high, and compacted over rejections with ballots and a
+// cross-warp prefix so the vertex order is exact.  estimate()'s trials therefore never cross PCIe:
 // seeds in, counts out.
 __device__ __forceinline__ uint64_t mt_temper(uint64_t x) {
   x ^= (x >> 29) & 0x5555555555555555ull;
@@ -335,14 +335,17 @@ __device__ __forceinline__ uint64_t mt_temper(uint64_t x) {
   x ^= x >> 43;
   return x;
 }
-__global__ void __launch_bounds__(32) k_random_colorings(const uint64_t* __restrict__ seeds, uint32_t n, uint32_t k,
-                                                         uint64_t limit, uint8_t* __restrict__ out) {
+constexpr int kRngThreads = 160;  // 5 warps: one thread per element of a half state (156)
+__global__ void __launch_bounds__(kRngThreads) k_random_colorings(const uint64_t* __restrict__ seeds, uint32_t n,
+                                                                  uint32_t k, uint64_t limit,
+                                                                  uint8_t* __restrict__ out) {
   constexpr int NN = 312, MM = 156;
   constexpr uint64_t UM = 0xFFFFFFFF80000000ull, LM = 0x7FFFFFFFull, MATRIX_A = 0xB5026F5AA96619E9ull;
   __shared__ uint64_t mt[NN];
-  const uint32_t lane = threadIdx.x;
+  __shared__ uint32_t s_cnt[kRngThreads / 32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   uint8_t* chi = out + static_cast<uint64_t>(blockIdx.x) * n;
-  if (lane == 0) {
+  if (tid == 0) {
     uint64_t x = seeds[blockIdx.x];
     mt[0] = x;
     for (int i = 1; i < NN; ++i) {
@@ -350,45 +353,50 @@ __global__ void __launch_bounds__(32) k_random_colorings(const uint64_t* __restr
       mt[i] = x;
     }
   }
-  __syncwarp();
+  __syncthreads();
   const uint64_t magic = k > 1 ? ~0ull / k : 0;  // floor((2^64 - 1) / k): quotient estimate low by at most 1
-  uint32_t v = 0;  // next vertex
+  uint32_t v = 0;  // next vertex (the same in every thread)
   while (v < n) {
-    // regenerate the state
+    // regenerate the state: each half in one step (reads of old words, barrier, writes)
     for (int half = 0; half < 2; ++half) {
-      const int lo = half * MM, hi = lo + MM;
-      for (int base = lo; base < hi; base += 32) {
-        const int i = base + lane;
-        uint64_t nx = 0;
-        if (i < hi) {
-          const uint64_t y = (mt[i] & UM) | (mt[(i + 1) % NN] & LM);
-          nx = mt[(i + MM) % NN] ^ (y >> 1) ^ ((y & 1ull) ? MATRIX_A : 0ull);
-        }
-        __syncwarp();  // every lane has read the old words of this step
-        if (i < hi) mt[i] = nx;
-        __syncwarp();
+      const int i = half * MM + static_cast<int>(tid);
+      uint64_t nx = 0;
+      if (tid < MM) {
+        const uint64_t y = (mt[i] & UM) | (mt[(i + 1) % NN] & LM);
+        nx = mt[(i + MM) % NN] ^ (y >> 1) ^ ((y & 1ull) ? MATRIX_A : 0ull);
       }
+      __syncthreads();
+      if (tid < MM) mt[i] = nx;
+      __syncthreads();
     }
-    // consume the 312 outputs in order
-    for (int base = 0; base < NN && v < n; base += 32) {
-      const int i = base + lane;
-      uint64_t x = i < NN ? mt_temper(mt[i]) : ~0ull;
+    // consume the 312 outputs in order, kRngThreads per step
+    for (int base = 0; base < NN && v < n; base += kRngThreads) {
+      const int i = base + static_cast<int>(tid);
+      const uint64_t x = i < NN ? mt_temper(mt[i]) : ~0ull;
       const bool ok = i < NN && x < limit;
       const unsigned acc = __ballot_sync(0xffffffffu, ok);
-      const uint32_t dst = v + __popc(acc & ((1u << lane) - 1u));
+      if (lane == 0) s_cnt[wid] = __popc(acc);
+      __syncthreads();
+      uint32_t before = 0, total = 0;
+#pragma unroll
+      for (int w = 0; w < kRngThreads / 32; ++w) {
+        const uint32_t c = s_cnt[w];
+        before += w < static_cast<int>(wid) ? c : 0u;
+        total += c;
+      }
+      const uint32_t dst = v + before + __popc(acc & ((1u << lane) - 1u));
       if (ok && dst < n) {
-        uint64_t r = x;
+        uint64_t r = 0;
         if (k > 1) {
           const uint64_t q = __umul64hi(x, magic);
           r = x - q * k;
           if (r >= k) r -= k;
           if (r >= k) r -= k;
-        } else {
-          r = 0;
         }
         chi[dst] = static_cast<uint8_t>(1 + r);
       }
-      v += __popc(acc);
+      v += total;
+      __syncthreads();  // s_cnt is rewritten by the next step
     }
   }
 }
